@@ -1,0 +1,179 @@
+/*
+ * fpm_b200.h — C-ABI of the B200-native FPM reconstruction engine.
+ *
+ * Drop-in boundary for the reference's per-tile reconstruction path
+ * (/root/reference/proj): run_offline -> reconstruct_tile -> update_step ->
+ * fft2/ifft2. The reference exposes that path as a C++ library API (no FFI
+ * layer exists); every entry point below names the reference function it
+ * replaces. Plain pointers and sizes only; no exceptions cross this boundary:
+ * every call returns an FPMGPU_* status and fpmgpu_last_error() holds the
+ * reference's message text (e.g. "missing frame", "spectrum offset out of
+ * canvas bounds", "pupil exceeds Nyquist").
+ *
+ * Arrays are row-major. Complex values are interleaved (re, im): complex64 as
+ * float[2], complex128 as double[2]. The reference's Eigen arrays are
+ * column-major; the C++ mirror (fpm_b200.hpp) converts.
+ */
+#ifndef FPM_B200_H
+#define FPM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPMGPU_OK 0
+#define FPMGPU_ERR_CONFIG 1      /* fpm::ConfigError          (optics.hpp:11-13)  */
+#define FPMGPU_ERR_DATA 2        /* fpm::DataError            (optics.hpp:14-16)  */
+#define FPMGPU_ERR_UNSAFE_LAG 3  /* fpm::UnsafeLagError       (parallel.hpp:12-17)*/
+#define FPMGPU_ERR_DOMAIN 4      /* std::domain_error         (optics.cpp:28-30)  */
+#define FPMGPU_ERR_CUDA 5        /* device / driver failure                        */
+#define FPMGPU_ERR_INTERNAL 6
+#define FPMGPU_ERR_UNSUPPORTED 7 /* geometry without a device kernel (tile side) */
+
+#define FPMGPU_MODE_GS 0   /* Gerchberg–Saxton replacement (recon.cpp:93-134) */
+#define FPMGPU_MODE_EPRY 1 /* + embedded pupil recovery (extension) */
+
+#define FPMGPU_ORDER_SPIRAL 0 /* UpdateOrder::Spiral (recon.hpp:12) */
+#define FPMGPU_ORDER_RASTER 1
+
+/* OpticalConfig (optics.hpp:29-52), same fields and units. */
+typedef struct fpmgpu_optical_config {
+    double wavelength, objective_na, magnification, camera_pixel, led_pitch;
+    int led_grid_rows, led_grid_cols;
+    double led_height;
+    int center_row, center_col, led_scan_rows, led_scan_cols, upsample, tile_size, tile_overlap;
+    double acq_pattern_delay, acq_exposure;
+} fpmgpu_optical_config;
+
+int fpmgpu_version(void);
+const char* fpmgpu_last_error(void);
+/* minimum lag carried by the last FPMGPU_ERR_UNSAFE_LAG (UnsafeLagError::minimum) */
+int fpmgpu_last_min_lag(void);
+/* fills the reference defaults (optics.hpp:30-45) */
+void fpmgpu_default_config(fpmgpu_optical_config* cfg);
+
+/* ---------------------------------------------------------------------------
+ * Host geometry: exact reference arithmetic in double. The device consumes
+ * only their integer outputs, so offsets, sub-aperture origins and the
+ * support disk are bit-exact against the reference by construction.
+ * ------------------------------------------------------------------------- */
+/* OpticalConfig::validate (optics.cpp:7-24) */
+int fpmgpu_validate_config(const fpmgpu_optical_config* cfg);
+/* illumination_wavevector (optics.cpp:26-39) */
+int fpmgpu_illumination_wavevector(const fpmgpu_optical_config* cfg, int led_row, int led_col,
+                                   double center_x_um, double center_y_um, double* fx, double* fy);
+/* build_pupil (optics.cpp:41-72); values: [grid][grid] complex128 or NULL */
+int fpmgpu_build_pupil(const fpmgpu_optical_config* cfg, int grid, double defocus_um,
+                       double* values, double* radius_px);
+/* synthesized_na (optics.cpp:74-85) */
+int fpmgpu_synthesized_na(const fpmgpu_optical_config* cfg, double* out);
+/* tile_origins (tiles.cpp:5-19); writes min(count, cap) origins */
+int fpmgpu_tile_origins(int fov, int tile_size, int tile_overlap, int* out, int cap, int* count);
+/* partition_tiles (tiles.cpp:21-48) restricted to the LEDs of `seq` ([L][2] (row, col)):
+ * xy [T][2] (x0, y0), centers [T][2] um, kvecs [T][L][2] (fx, fy), offsets [T][L][2]
+ * (oy, ox) = spectrum_offset_px (recon.cpp:50-53). Any output may be NULL. */
+int fpmgpu_partition_tiles(const fpmgpu_optical_config* cfg, int fov_w, int fov_h,
+                           const int* seq, int num_leds, int cap, int* count, int* xy,
+                           double* centers, double* kvecs, int* offsets);
+/* sequence_offsets (recon.cpp:15-41): out [rows*cols][2] (dr, dc) */
+int fpmgpu_sequence_offsets(int order, int rows, int cols, int* out);
+/* spectrum_offset_px (recon.cpp:50-53) */
+int fpmgpu_spectrum_offset_px(const fpmgpu_optical_config* cfg, double fx, double fy, int* oy,
+                              int* ox);
+/* min_safe_lag (parallel.cpp:17-29) */
+int fpmgpu_min_safe_lag(const int* offsets, int count, double radius_px, int* out);
+/* build_schedule (parallel.cpp:39-50): entries [positions*iters][3] (round, stage, position) */
+int fpmgpu_build_schedule(int positions, int iters, int lag, int* entries, int* rounds);
+
+/* ---------------------------------------------------------------------------
+ * Device engine.
+ * ------------------------------------------------------------------------- */
+typedef struct fpmgpu_context fpmgpu_context;
+typedef struct fpmgpu_plan fpmgpu_plan;
+
+int fpmgpu_create(int device, fpmgpu_context** out);
+int fpmgpu_destroy(fpmgpu_context* ctx);
+
+/* One batched reconstruction: T tiles of one FOV, each the reference's
+ * reconstruct_tile (recon.cpp:141-170) — or pipelined_reconstruct_tile
+ * (parallel.cpp:52-111) when lag != 0 — followed by canvas_to_field. */
+typedef struct fpmgpu_recon_request {
+    fpmgpu_optical_config cfg; /* tile_size = n (LR side), upsample: N = n*upsample */
+    int iters;                 /* passes over the sequence (>= 1) */
+    int mode;                  /* FPMGPU_MODE_GS | FPMGPU_MODE_EPRY */
+    double alpha, beta;        /* EPRY step sizes (ignored for GS) */
+    int lag;                   /* 0 sequential; > 0 pipelined at this lag; -1 pipelined, auto lag */
+    int force_unsafe_lag;      /* run a lag below min_safe_lag (result nondeterministic) */
+    int num_tiles;             /* T */
+    const int* tile_xy;        /* [T][2] (x0, y0) LR origin of each tile in the frames */
+    int num_leds;              /* L (sequence length) */
+    const int* offsets;        /* [T][L][2] (oy, ox) spectrum offsets in sequence order */
+    const int* seq_frame;      /* [L] frame index of sequence position k */
+    int init_frame;            /* frame seeding init_canvas (on-axis, else brightest) */
+    const double* tile_defocus_um; /* [T] per-tile defocus for build_pupil, or NULL (0) */
+    const float* pupils;       /* [T][n][n] complex64 initial pupils or NULL (built) */
+    int num_frames, height, width; /* LR stack geometry: frames [F][H][W] u16 */
+} fpmgpu_recon_request;
+
+/* Host-buffer call (the reference-facing path): frames [F][H][row_pitch] u16 in
+ * host memory; outputs to host memory (any may be NULL): hr [T][N][N]
+ * complex64 (canvas_to_field units), residuals [T][iters]
+ * (pass_mean_residual), pupils_out [T][n][n] complex64. Copies in/out are
+ * part of the call. */
+int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* req,
+                             const uint16_t* frames, int64_t row_pitch, float* hr,
+                             double* residuals, float* pupils_out, int* lag_used);
+
+/* Plans: validate + upload the geometry tables once, then execute on device
+ * buffers (frames/hr/residuals/pupils_out are DEVICE pointers; row_pitch in
+ * elements, row_pitch*2 must be a multiple of 16 bytes). `stream` is a
+ * cudaStream_t (NULL = legacy default). */
+int fpmgpu_plan_create(fpmgpu_context* ctx, const fpmgpu_recon_request* req, fpmgpu_plan** out);
+int fpmgpu_plan_execute(fpmgpu_plan* plan, const uint16_t* frames_dev, int64_t row_pitch,
+                        float* hr_dev, double* residuals_dev, float* pupils_out_dev, void* stream);
+int fpmgpu_plan_destroy(fpmgpu_plan* plan);
+
+typedef struct fpmgpu_plan_info {
+    int tile_side, canvas_side, num_tiles, num_leds, iters, mode, lag, groups;
+    int launches_per_execute;   /* kernels launched by one fpmgpu_plan_execute */
+    int loop_ctas, loop_threads, loop_smem_bytes;
+    double updates;             /* T * L * iters */
+    double fft_flops_per_update;  /* 20 n^2 log2 n (nominal) */
+    double hbm_bytes_per_update;  /* 2 n^2 + 16 |D| */
+    int support_pixels;         /* |D| */
+} fpmgpu_plan_info;
+int fpmgpu_plan_get_info(const fpmgpu_plan* plan, fpmgpu_plan_info* info);
+
+/* Device time of each phase, summed over the executes recorded since the last
+ * reset (CUDA events on the execute stream around every phase): ms[0] pupils +
+ * init_canvas, ms[1] LED loop kernel, ms[2] canvas_to_field. Call after the
+ * stream has been synchronised; reset != 0 clears the record afterwards. */
+int fpmgpu_plan_phase_times(fpmgpu_plan* plan, double* ms, int* executes, int reset);
+
+/* Single alternating-projection step on a host canvas (update_step,
+ * recon.cpp:93-134; EPRY step when mode = EPRY, pupil updated in place).
+ * canvas [N][N] complex64 in/out, intensity [n][n] float, pupil [n][n]
+ * complex64 (in/out for EPRY). Support = pupil != 0 on entry. */
+int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, float* canvas,
+                       const float* intensity, double fx, double fy, float* pupil, int mode,
+                       double alpha, double beta, double* residual);
+
+/* init_canvas (recon.cpp:61-86) for one tile from frame [H][row_pitch] u16 at
+ * (x0, y0); canvas_to_field (recon.cpp:88-91). Host buffers, complex64. */
+int fpmgpu_init_canvas(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg,
+                       const uint16_t* frame, int height, int width, int64_t row_pitch, int x0,
+                       int y0, float* canvas);
+int fpmgpu_canvas_to_field(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg,
+                           const float* canvas, float* field);
+
+/* stitch_mosaic (stitch.cpp:48-86) of T HR tiles [T][N][N] complex64 (host) at LR
+ * origins xy [T][2]; out [rows][cols] complex64 (host) or NULL to query the size. */
+int fpmgpu_stitch_mosaic(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const float* tiles,
+                         const int* xy, int num_tiles, float* out, int* rows, int* cols);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPM_B200_H */

@@ -1,0 +1,762 @@
+// C-ABI of the B200 FPM engine (include/fpm_b200.h): host geometry, plans,
+// launches. No exception crosses the boundary; see guarded().
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fpm_b200.h"
+#include "geometry.hpp"
+#include "kernels.cuh"
+
+using namespace fpmb;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_min_lag = 0;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FPMGPU_OK;
+    } catch (const UnsafeLag& e) {
+        g_err = e.what();
+        g_min_lag = e.minimum;
+        return FPMGPU_ERR_UNSAFE_LAG;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return FPMGPU_ERR_CONFIG;
+    } catch (const DataError& e) {
+        g_err = e.what();
+        return FPMGPU_ERR_DATA;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return FPMGPU_ERR_DOMAIN;
+    } catch (const Unsupported& e) {
+        g_err = e.what();
+        return FPMGPU_ERR_UNSUPPORTED;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return FPMGPU_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FPMGPU_ERR_INTERNAL;
+    }
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* ensure(size_t count) {
+        if (count > n) {
+            reset();
+            ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+            n = count;
+        }
+        return p;
+    }
+    void upload(const T* h, size_t count, cudaStream_t s) {
+        ensure(count);
+        ck(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    }
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 3-D map over the LR stack [F][H][pitch] u16 with a 64x64x1 box, 128B swizzle.
+CUtensorMap encode_frames_map(const uint16_t* frames, int F, int H, int W, int64_t pitch) {
+    if ((pitch * 2) % 16 != 0) throw DataError("frame row pitch must be a multiple of 8 elements");
+    if (reinterpret_cast<uintptr_t>(frames) % 16 != 0) throw DataError("frame base must be 16-byte aligned");
+    CUtensorMap m;
+    cuuint64_t dims[3] = {cuuint64_t(W), cuuint64_t(H), cuuint64_t(F)};
+    cuuint64_t strides[2] = {cuuint64_t(pitch) * 2, cuuint64_t(pitch) * 2 * cuuint64_t(H)};
+    cuuint32_t box[3] = {64, 64, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t*>(frames), dims,
+                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+// Support-dependent kernel shape: compact pupil slots per thread and whether
+// the disk lies inside the pruned lattice rows/cols [16, 48).
+void lattice_shape(const std::vector<uint8_t>& support, int* nslots, bool* prune) {
+    int mx = 0;
+    bool inside = true;
+    for (int t = 0; t < 64; ++t) {
+        int c = 0;
+        for (int a = 0; a < 8; ++a)
+            for (int b = 0; b < 8; ++b) {
+                const int i = (t >> 3) + 8 * a, j = (t & 7) + 8 * b;
+                if (support[size_t(i) * 64 + j]) {
+                    ++c;
+                    if (a < 2 || a > 5 || b < 2 || b > 5) inside = false;
+                }
+            }
+        mx = std::max(mx, c);
+    }
+    *nslots = std::max(mx, 1);
+    *prune = inside;
+}
+
+std::vector<float2> twiddles(int N) {
+    std::vector<float2> w(static_cast<size_t>(N));
+    for (int m = 0; m < N; ++m) {
+        const double a = -2.0 * 3.14159265358979323846 * double(m) / double(N);
+        w[size_t(m)] = make_float2(float(std::cos(a)), float(std::sin(a)));
+    }
+    return w;
+}
+
+}  // namespace
+
+struct fpmgpu_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf<float2> tw256, tw512, tw1024;
+    // host-path staging
+    DevBuf<uint16_t> frames;
+    DevBuf<float2> hr;
+    DevBuf<double> resid;
+    DevBuf<float2> pup;
+    fpmgpu_plan* cached = nullptr;
+    std::vector<int> cached_key_i;
+    std::vector<double> cached_key_d;
+    std::vector<float> cached_key_f;
+
+    const float2* twiddle_table(int N) {
+        DevBuf<float2>* b = N == 256 ? &tw256 : N == 512 ? &tw512 : N == 1024 ? &tw1024 : nullptr;
+        if (!b) throw Unsupported("canvas side " + std::to_string(N) + " has no line-FFT kernel (256/512/1024)");
+        if (!b->p) {
+            auto w = twiddles(N);
+            b->upload(w.data(), w.size(), stream);
+        }
+        return b->p;
+    }
+};
+
+struct fpmgpu_plan {
+    fpmgpu_context* ctx = nullptr;
+    fpmgpu_recon_request req{};
+    int n = 0, N = 0, T = 0, L = 0, F = 0, G = 1, lag = 0, nslots = 1, num_slots = 0;
+    bool prune = false;
+    int support_px = 0;
+    double radius = 0.0;
+    DevBuf<float2> canvas, pupils, pupils_init;
+    DevBuf<uint8_t> support;
+    DevBuf<short2> origins;
+    DevBuf<int> seq_frame;
+    DevBuf<int2> tile_xy, slots;
+    DevBuf<double> defocus, resid;
+    bool has_defocus = false, has_pupils = false;
+    // phase events of recent executes: [slot][4] = start, after init, after loop, after finalize
+    static constexpr int kEventSlots = 256;
+    std::vector<cudaEvent_t> events;
+    int recorded = 0;
+    ~fpmgpu_plan() {
+        for (auto e : events) cudaEventDestroy(e);
+    }
+    cudaEvent_t* slot_events() {
+        if (events.empty()) {
+            events.resize(size_t(kEventSlots) * 4);
+            for (auto& e : events) ck(cudaEventCreate(&e), "cudaEventCreate");
+        }
+        if (recorded >= kEventSlots) return nullptr;
+        return events.data() + size_t(recorded++) * 4;
+    }
+};
+
+namespace {
+
+void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
+    const Cfg& c = r.cfg;
+    validate(c);
+    if (r.iters < 1) throw ConfigError("iters must be >= 1");
+    if (r.mode != FPMGPU_MODE_GS && r.mode != FPMGPU_MODE_EPRY) throw ConfigError("unknown reconstruction mode");
+    p.req = r;
+    p.n = c.tile_size;
+    p.N = c.tile_size * c.upsample;
+    p.T = r.num_tiles;
+    p.L = r.num_leds;
+    p.F = r.num_frames;
+    if (p.T < 1) throw ConfigError("no tiles to reconstruct");
+    if (p.L < 1) throw DataError("min_safe_lag: empty sequence");
+    p.radius = pupil_radius_px(c, p.n);  // ConfigError on Nyquist / grid checks
+    if (p.n != 64)
+        throw Unsupported("tile side " + std::to_string(p.n) + " has no device kernel in this build (n = 64)");
+    if (p.N != 256 && p.N != 512 && p.N != 1024)
+        throw Unsupported("canvas side " + std::to_string(p.N) + " has no line-FFT kernel (256/512/1024)");
+    for (int t = 0; t < p.T; ++t) {
+        const int x0 = r.tile_xy[2 * t], y0 = r.tile_xy[2 * t + 1];
+        if (x0 < 0 || y0 < 0 || y0 + p.n > r.height || x0 + p.n > r.width)
+            throw DataError("tile extends past frame bounds");
+    }
+    if (r.init_frame < 0 || r.init_frame >= p.F) throw DataError("empty frame set");
+    for (int k = 0; k < p.L; ++k)
+        if (r.seq_frame[k] < 0 || r.seq_frame[k] >= p.F)
+            throw DataError("missing frame for sequence position " + std::to_string(k));
+
+    std::vector<short2> org(size_t(p.T) * p.L);
+    for (int t = 0; t < p.T; ++t)
+        for (int k = 0; k < p.L; ++k) {
+            const int oy = r.offsets[(size_t(t) * p.L + k) * 2], ox = r.offsets[(size_t(t) * p.L + k) * 2 + 1];
+            const int r0 = p.N / 2 + oy - p.n / 2, c0 = p.N / 2 + ox - p.n / 2;
+            if (r0 < 0 || c0 < 0 || r0 + p.n > p.N || c0 + p.n > p.N)
+                throw DataError("spectrum offset out of canvas bounds");
+            org[size_t(t) * p.L + k] = make_short2(short(r0), short(c0));
+        }
+
+    std::vector<uint8_t> sup = support_disk(p.n, p.radius);
+    p.support_px = 0;
+    for (auto s : sup) p.support_px += s;
+    lattice_shape(sup, &p.nslots, &p.prune);
+
+    // pipelined schedule (parallel.cpp:52-111): one lag for the whole batch,
+    // the largest per-tile minimum, so every tile stays sequential-equivalent
+    std::vector<int2> slots;
+    p.G = 1;
+    p.lag = 0;
+    if (r.lag != 0) {
+        if (r.mode != FPMGPU_MODE_GS) throw ConfigError("pipelined schedule requires Gerchberg-Saxton mode");
+        int min_lag = 1;
+        for (int t = 0; t < p.T; ++t) {
+            std::vector<std::pair<int, int>> offs;
+            for (int k = 0; k < p.L; ++k)
+                offs.emplace_back(r.offsets[(size_t(t) * p.L + k) * 2], r.offsets[(size_t(t) * p.L + k) * 2 + 1]);
+            min_lag = std::max(min_lag, min_safe_lag(offs, p.radius));
+        }
+        const int use = r.lag < 0 ? min_lag : r.lag;
+        if (use < min_lag && !r.force_unsafe_lag) throw UnsafeLag(min_lag);
+        p.lag = use;
+        const int R = (p.L - 1) + (r.iters - 1) * use + 1;
+        std::vector<std::vector<int2>> rounds(static_cast<size_t>(R));
+        for (int s = 0; s < r.iters; ++s)
+            for (int q = 0; q < p.L; ++q) rounds[size_t(q + s * use)].push_back(make_int2(s, q));
+        size_t widest = 1;
+        for (auto& rd : rounds) widest = std::max(widest, rd.size());
+        p.G = widest > 1 ? 2 : 1;
+        if (p.G > 1) {
+            for (auto& rd : rounds)
+                for (size_t c0 = 0; c0 < rd.size(); c0 += 2)
+                    for (int g = 0; g < 2; ++g)
+                        slots.push_back(c0 + g < rd.size() ? rd[c0 + g] : make_int2(-1, -1));
+        }
+    }
+    p.num_slots = p.G == 1 ? r.iters * p.L : int(slots.size() / 2);
+
+    cudaStream_t s = p.ctx->stream;
+    p.support.upload(sup.data(), sup.size(), s);
+    p.origins.upload(org.data(), org.size(), s);
+    p.seq_frame.upload(r.seq_frame, size_t(p.L), s);
+    std::vector<int2> xy(static_cast<size_t>(p.T));
+    for (int t = 0; t < p.T; ++t) xy[size_t(t)] = make_int2(r.tile_xy[2 * t], r.tile_xy[2 * t + 1]);
+    p.tile_xy.upload(xy.data(), xy.size(), s);
+    if (p.G > 1) p.slots.upload(slots.data(), slots.size(), s);
+    p.has_defocus = r.tile_defocus_um != nullptr;
+    if (p.has_defocus) p.defocus.upload(r.tile_defocus_um, size_t(p.T), s);
+    p.has_pupils = r.pupils != nullptr;
+    if (p.has_pupils)
+        p.pupils_init.upload(reinterpret_cast<const float2*>(r.pupils), size_t(p.T) * p.n * p.n, s);
+    p.canvas.ensure(size_t(p.T) * p.N * p.N);
+    p.pupils.ensure(size_t(p.T) * p.n * p.n);
+    p.resid.ensure(size_t(p.T) * r.iters);
+    p.ctx->twiddle_table(p.N);
+    // the request's host arrays belong to the caller; keep only scalars
+    p.req.tile_xy = nullptr;
+    p.req.offsets = nullptr;
+    p.req.seq_frame = nullptr;
+    p.req.tile_defocus_um = nullptr;
+    p.req.pupils = nullptr;
+}
+
+void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* hr, double* resid,
+                  float* pupils_out, cudaStream_t s) {
+    const fpmgpu_recon_request& r = p.req;
+    const CUtensorMap map = encode_frames_map(frames, p.F, r.height, r.width, pitch);
+    cudaEvent_t* ev = p.slot_events();
+    if (ev) ck(cudaEventRecord(ev[0], s), "event");
+    const double dk = 1.0 / (p.n * dx_obj(r.cfg));
+    const double inv_l2 = 1.0 / (r.cfg.wavelength * r.cfg.wavelength);
+    // pupils (build_pupil per tile, or the caller's)
+    if (p.has_pupils)
+        ck(cudaMemcpyAsync(p.pupils.p, p.pupils_init.p, sizeof(float2) * size_t(p.T) * p.n * p.n,
+                           cudaMemcpyDeviceToDevice, s), "pupil copy");
+    else
+        ck(fpmk::launch_build_pupils(p.pupils.p, p.support.p, p.has_defocus ? p.defocus.p : nullptr, p.n, p.T, dk,
+                                     inv_l2, s), "build_pupils");
+    // init_canvas: bilinear(sqrt(seed crop)) -> centered FFT N x N -> / up^2
+    fpmk::LinesArgs la{};
+    la.tw = p.ctx->twiddle_table(p.N);
+    la.frame = frames + size_t(r.init_frame) * size_t(r.height) * size_t(pitch);
+    la.pitch = pitch;
+    la.tile_xy = p.tile_xy.p;
+    la.n = p.n;
+    la.up = r.cfg.upsample;
+    la.src = p.canvas.p;
+    la.dst = p.canvas.p;
+    la.scale = 1.0f;
+    ck(fpmk::launch_lines(0, p.N, la, p.T, s), "init rows");
+    la.scale = float(1.0 / (double(r.cfg.upsample) * r.cfg.upsample));
+    ck(fpmk::launch_lines(1, p.N, la, p.T, s), "init cols");
+    if (ev) ck(cudaEventRecord(ev[1], s), "event");
+    // the LED loop
+    fpmk::LoopArgs a{};
+    a.canvas = p.canvas.p;
+    a.pupils = p.pupils.p;
+    a.support = p.support.p;
+    a.origins = p.origins.p;
+    a.seq_frame = p.seq_frame.p;
+    a.tile_xy = p.tile_xy.p;
+    a.residuals = resid ? resid : p.resid.p;
+    a.slots = p.G > 1 ? p.slots.p : nullptr;
+    a.num_slots = p.num_slots;
+    a.T = p.T;
+    a.L = p.L;
+    a.iters = r.iters;
+    a.N = p.N;
+    a.nslots = p.nslots;
+    a.alpha = float(r.alpha);
+    a.beta = float(r.beta);
+    ck(fpmk::launch_loop64(r.mode, p.prune, fpmk::kMeasTMA, p.G, &map, a, p.T, s), "LED loop");
+    if (ev) ck(cudaEventRecord(ev[2], s), "event");
+    // canvas_to_field: centered IFFT N x N * up^2 (the 1/N^2 of ifft2 folded in)
+    la.src = p.canvas.p;
+    la.dst = p.canvas.p;
+    la.scale = 1.0f;
+    ck(fpmk::launch_lines(2, p.N, la, p.T, s), "final rows");
+    la.dst = hr ? reinterpret_cast<float2*>(hr) : p.canvas.p;
+    la.scale = float(double(r.cfg.upsample) * r.cfg.upsample / (double(p.N) * p.N));
+    ck(fpmk::launch_lines(3, p.N, la, p.T, s), "final cols");
+    if (ev) ck(cudaEventRecord(ev[3], s), "event");
+    if (pupils_out)
+        ck(cudaMemcpyAsync(pupils_out, p.pupils.p, sizeof(float2) * size_t(p.T) * p.n * p.n,
+                           cudaMemcpyDeviceToDevice, s), "pupil out");
+}
+
+bool same_request(const fpmgpu_context& c, const fpmgpu_recon_request& r, std::vector<int>& ki,
+                  std::vector<double>& kd, std::vector<float>& kf) {
+    ki.clear();
+    kd.clear();
+    kf.clear();
+    const int* cfg_i = reinterpret_cast<const int*>(&r.cfg);
+    ki.insert(ki.end(), cfg_i, cfg_i + sizeof(r.cfg) / sizeof(int));
+    ki.insert(ki.end(), {r.iters, r.mode, r.lag, r.force_unsafe_lag, r.num_tiles, r.num_leds, r.init_frame,
+                         r.num_frames, r.height, r.width});
+    ki.insert(ki.end(), r.tile_xy, r.tile_xy + 2 * size_t(r.num_tiles));
+    ki.insert(ki.end(), r.offsets, r.offsets + 2 * size_t(r.num_tiles) * r.num_leds);
+    ki.insert(ki.end(), r.seq_frame, r.seq_frame + r.num_leds);
+    kd.push_back(r.alpha);
+    kd.push_back(r.beta);
+    if (r.tile_defocus_um) kd.insert(kd.end(), r.tile_defocus_um, r.tile_defocus_um + r.num_tiles);
+    if (r.pupils) kf.insert(kf.end(), r.pupils, r.pupils + 2 * size_t(r.num_tiles) * r.cfg.tile_size * r.cfg.tile_size);
+    return c.cached && ki == c.cached_key_i && kd == c.cached_key_d && kf == c.cached_key_f;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fpmgpu_version(void) { return 1; }
+const char* fpmgpu_last_error(void) { return g_err.c_str(); }
+int fpmgpu_last_min_lag(void) { return g_min_lag; }
+void fpmgpu_default_config(fpmgpu_optical_config* cfg) { default_config(*cfg); }
+
+int fpmgpu_validate_config(const fpmgpu_optical_config* cfg) { return guarded([&] { validate(*cfg); }); }
+
+int fpmgpu_illumination_wavevector(const fpmgpu_optical_config* cfg, int led_row, int led_col, double cx,
+                                   double cy, double* fx, double* fy) {
+    return guarded([&] {
+        auto k = wavevector(*cfg, led_row, led_col, cx, cy);
+        *fx = k.first;
+        *fy = k.second;
+    });
+}
+
+int fpmgpu_build_pupil(const fpmgpu_optical_config* cfg, int grid, double defocus_um, double* values,
+                       double* radius_px) {
+    return guarded([&] {
+        auto v = build_pupil(*cfg, grid, defocus_um, radius_px);
+        if (values) std::memcpy(values, v.data(), v.size() * sizeof(double));
+    });
+}
+
+int fpmgpu_synthesized_na(const fpmgpu_optical_config* cfg, double* out) {
+    return guarded([&] { *out = synthesized_na(*cfg); });
+}
+
+int fpmgpu_tile_origins(int fov, int tile_size, int tile_overlap, int* out, int cap, int* count) {
+    return guarded([&] {
+        auto v = tile_origins(fov, tile_size, tile_overlap);
+        *count = int(v.size());
+        for (int i = 0; i < int(v.size()) && i < cap; ++i) out[i] = v[size_t(i)];
+    });
+}
+
+int fpmgpu_partition_tiles(const fpmgpu_optical_config* cfg, int fov_w, int fov_h, const int* seq, int num_leds,
+                           int cap, int* count, int* xy, double* centers, double* kvecs, int* offsets) {
+    return guarded([&] {
+        const auto xs = tile_origins(fov_w, cfg->tile_size, cfg->tile_overlap);
+        const auto ys = tile_origins(fov_h, cfg->tile_size, cfg->tile_overlap);
+        *count = int(xs.size() * ys.size());
+        int t = 0;
+        for (int y0 : ys)
+            for (int x0 : xs) {
+                if (t >= cap) return;
+                auto [cx, cy] = tile_center_um(*cfg, x0, y0, fov_w, fov_h);
+                if (xy) {
+                    xy[2 * t] = x0;
+                    xy[2 * t + 1] = y0;
+                }
+                if (centers) {
+                    centers[2 * t] = cx;
+                    centers[2 * t + 1] = cy;
+                }
+                for (int k = 0; k < num_leds; ++k) {
+                    auto [fx, fy] = wavevector(*cfg, seq[2 * k], seq[2 * k + 1], cx, cy);
+                    const size_t q = (size_t(t) * num_leds + k) * 2;
+                    if (kvecs) {
+                        kvecs[q] = fx;
+                        kvecs[q + 1] = fy;
+                    }
+                    if (offsets) {
+                        auto [oy, ox] = spectrum_offset_px(*cfg, fx, fy);
+                        offsets[q] = oy;
+                        offsets[q + 1] = ox;
+                    }
+                }
+                ++t;
+            }
+    });
+}
+
+int fpmgpu_sequence_offsets(int order, int rows, int cols, int* out) {
+    return guarded([&] {
+        auto v = sequence_offsets(order, rows, cols);
+        for (size_t i = 0; i < v.size(); ++i) {
+            out[2 * i] = v[i].first;
+            out[2 * i + 1] = v[i].second;
+        }
+    });
+}
+
+int fpmgpu_spectrum_offset_px(const fpmgpu_optical_config* cfg, double fx, double fy, int* oy, int* ox) {
+    return guarded([&] {
+        auto o = spectrum_offset_px(*cfg, fx, fy);
+        *oy = o.first;
+        *ox = o.second;
+    });
+}
+
+int fpmgpu_min_safe_lag(const int* offsets, int count, double radius_px, int* out) {
+    return guarded([&] {
+        std::vector<std::pair<int, int>> v;
+        for (int i = 0; i < count; ++i) v.emplace_back(offsets[2 * i], offsets[2 * i + 1]);
+        *out = min_safe_lag(v, radius_px);
+    });
+}
+
+int fpmgpu_build_schedule(int positions, int iters, int lag, int* entries, int* rounds) {
+    return guarded([&] {
+        if (positions < 1 || iters < 1 || lag < 1) throw ConfigError("invalid schedule parameters");
+        const int R = (positions - 1) + (iters - 1) * lag + 1;
+        *rounds = R;
+        size_t q = 0;
+        for (int r = 0; r < R; ++r)
+            for (int s = 0; s < iters; ++s) {
+                const int p = r - s * lag;
+                if (p < 0 || p >= positions) continue;
+                entries[3 * q] = r;
+                entries[3 * q + 1] = s;
+                entries[3 * q + 2] = p;
+                ++q;
+            }
+    });
+}
+
+int fpmgpu_create(int device, fpmgpu_context** out) {
+    return guarded([&] {
+        auto c = std::make_unique<fpmgpu_context>();
+        c->device = device;
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        *out = c.release();
+    });
+}
+
+int fpmgpu_destroy(fpmgpu_context* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        if (ctx->cached) delete ctx->cached;
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int fpmgpu_plan_create(fpmgpu_context* ctx, const fpmgpu_recon_request* req, fpmgpu_plan** out) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        auto p = std::make_unique<fpmgpu_plan>();
+        p->ctx = ctx;
+        build_plan(*p, *req);
+        ck(cudaStreamSynchronize(ctx->stream), "plan upload");
+        *out = p.release();
+    });
+}
+
+int fpmgpu_plan_execute(fpmgpu_plan* plan, const uint16_t* frames_dev, int64_t row_pitch, float* hr_dev,
+                        double* residuals_dev, float* pupils_out_dev, void* stream) {
+    return guarded([&] {
+        execute_plan(*plan, frames_dev, row_pitch, hr_dev, residuals_dev, pupils_out_dev,
+                     static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fpmgpu_plan_destroy(fpmgpu_plan* plan) {
+    return guarded([&] { delete plan; });
+}
+
+int fpmgpu_plan_get_info(const fpmgpu_plan* p, fpmgpu_plan_info* info) {
+    return guarded([&] {
+        std::memset(info, 0, sizeof(*info));
+        info->tile_side = p->n;
+        info->canvas_side = p->N;
+        info->num_tiles = p->T;
+        info->num_leds = p->L;
+        info->iters = p->req.iters;
+        info->mode = p->req.mode;
+        info->lag = p->lag;
+        info->groups = p->G;
+        info->launches_per_execute = (p->has_pupils ? 0 : 1) + 2 + 1 + 2;
+        info->loop_ctas = p->T;
+        info->loop_threads = 64 * p->G;
+        info->loop_smem_bytes = int(fpmk::loop_smem_bytes(p->G, p->nslots, p->L, p->req.iters));
+        info->updates = double(p->T) * p->L * p->req.iters;
+        info->fft_flops_per_update = 20.0 * p->n * p->n * std::log2(double(p->n));
+        info->hbm_bytes_per_update = 2.0 * p->n * p->n + 16.0 * p->support_px;
+        info->support_pixels = p->support_px;
+    });
+}
+
+int fpmgpu_plan_phase_times(fpmgpu_plan* plan, double* ms, int* executes, int reset) {
+    return guarded([&] {
+        ms[0] = ms[1] = ms[2] = 0.0;
+        for (int k = 0; k < plan->recorded; ++k) {
+            cudaEvent_t* e = plan->events.data() + size_t(k) * 4;
+            for (int ph = 0; ph < 3; ++ph) {
+                float t = 0.f;
+                ck(cudaEventElapsedTime(&t, e[ph], e[ph + 1]), "cudaEventElapsedTime");
+                ms[ph] += t;
+            }
+        }
+        *executes = plan->recorded;
+        if (reset) plan->recorded = 0;
+    });
+}
+
+int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames,
+                             int64_t row_pitch, float* hr, double* residuals, float* pupils_out, int* lag_used) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        cudaStream_t s = ctx->stream;
+        std::vector<int> ki;
+        std::vector<double> kd;
+        std::vector<float> kf;
+        if (!same_request(*ctx, *req, ki, kd, kf)) {
+            auto p = std::make_unique<fpmgpu_plan>();
+            p->ctx = ctx;
+            build_plan(*p, *req);
+            if (ctx->cached) delete ctx->cached;
+            ctx->cached = p.release();
+            ctx->cached_key_i.swap(ki);
+            ctx->cached_key_d.swap(kd);
+            ctx->cached_key_f.swap(kf);
+        }
+        fpmgpu_plan& p = *ctx->cached;
+        const int W = req->width, H = req->height, F = req->num_frames;
+        const int64_t pitch = (int64_t(W) + 63) / 64 * 64;
+        uint16_t* fd = ctx->frames.ensure(size_t(F) * H * pitch);
+        ck(cudaMemcpy2DAsync(fd, size_t(pitch) * 2, frames, size_t(row_pitch) * 2, size_t(W) * 2, size_t(F) * H,
+                             cudaMemcpyHostToDevice, s), "frames H2D");
+        const size_t hr_n = size_t(p.T) * p.N * p.N, pup_n = size_t(p.T) * p.n * p.n;
+        float2* hr_d = hr ? ctx->hr.ensure(hr_n) : nullptr;
+        double* res_d = ctx->resid.ensure(size_t(p.T) * req->iters);
+        float2* pup_d = pupils_out ? ctx->pup.ensure(pup_n) : nullptr;
+        execute_plan(p, fd, pitch, reinterpret_cast<float*>(hr_d), res_d, reinterpret_cast<float*>(pup_d), s);
+        if (hr) ck(cudaMemcpyAsync(hr, hr_d, hr_n * sizeof(float2), cudaMemcpyDeviceToHost, s), "hr D2H");
+        if (residuals)
+            ck(cudaMemcpyAsync(residuals, res_d, sizeof(double) * size_t(p.T) * req->iters, cudaMemcpyDeviceToHost, s),
+               "residual D2H");
+        if (pupils_out) ck(cudaMemcpyAsync(pupils_out, pup_d, pup_n * sizeof(float2), cudaMemcpyDeviceToHost, s), "pupil D2H");
+        ck(cudaStreamSynchronize(s), "reconstruct");
+        if (lag_used) *lag_used = p.lag;
+    });
+}
+
+int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, float* canvas, const float* intensity,
+                       double fx, double fy, float* pupil, int mode, double alpha, double beta, double* residual) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int n = cfg->tile_size, N = cfg->tile_size * cfg->upsample;
+        if (n != 64) throw Unsupported("tile side " + std::to_string(n) + " has no device kernel in this build (n = 64)");
+        auto [oy, ox] = spectrum_offset_px(*cfg, fx, fy);
+        const int r0 = N / 2 + oy - n / 2, c0 = N / 2 + ox - n / 2;
+        if (r0 < 0 || c0 < 0 || r0 + n > N || c0 + n > N) throw DataError("spectrum offset out of canvas bounds");
+        std::vector<uint8_t> sup(size_t(n) * n);
+        for (size_t i = 0; i < sup.size(); ++i) sup[i] = pupil[2 * i] != 0.f || pupil[2 * i + 1] != 0.f;
+        int nslots;
+        bool prune;
+        lattice_shape(sup, &nslots, &prune);
+        cudaStream_t s = ctx->stream;
+        DevBuf<float2> cv, pp;
+        DevBuf<float> meas;
+        DevBuf<uint8_t> sp;
+        DevBuf<short2> org;
+        DevBuf<int> sf;
+        DevBuf<int2> xy;
+        DevBuf<double> res;
+        cv.upload(reinterpret_cast<const float2*>(canvas), size_t(N) * N, s);
+        pp.upload(reinterpret_cast<const float2*>(pupil), size_t(n) * n, s);
+        meas.upload(intensity, size_t(n) * n, s);
+        sp.upload(sup.data(), sup.size(), s);
+        const short2 o = make_short2(short(r0), short(c0));
+        org.upload(&o, 1, s);
+        const int zero = 0;
+        sf.upload(&zero, 1, s);
+        const int2 z2 = make_int2(0, 0);
+        xy.upload(&z2, 1, s);
+        res.ensure(1);
+        fpmk::LoopArgs a{};
+        a.canvas = cv.p;
+        a.pupils = pp.p;
+        a.support = sp.p;
+        a.origins = org.p;
+        a.seq_frame = sf.p;
+        a.tile_xy = xy.p;
+        a.residuals = res.p;
+        a.meas_f32 = meas.p;
+        a.num_slots = 1;
+        a.T = 1;
+        a.L = 1;
+        a.iters = 1;
+        a.N = N;
+        a.nslots = nslots;
+        a.alpha = float(alpha);
+        a.beta = float(beta);
+        CUtensorMap dummy;
+        std::memset(&dummy, 0, sizeof(dummy));
+        ck(fpmk::launch_loop64(mode, prune, fpmk::kMeasF32, 1, &dummy, a, 1, s), "update_step");
+        ck(cudaMemcpyAsync(canvas, cv.p, sizeof(float2) * size_t(N) * N, cudaMemcpyDeviceToHost, s), "canvas D2H");
+        if (mode == FPMGPU_MODE_EPRY)
+            ck(cudaMemcpyAsync(pupil, pp.p, sizeof(float2) * size_t(n) * n, cudaMemcpyDeviceToHost, s), "pupil D2H");
+        ck(cudaMemcpyAsync(residual, res.p, sizeof(double), cudaMemcpyDeviceToHost, s), "residual D2H");
+        ck(cudaStreamSynchronize(s), "update_step");
+    });
+}
+
+int fpmgpu_init_canvas(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const uint16_t* frame, int height,
+                       int width, int64_t row_pitch, int x0, int y0, float* canvas) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        validate(*cfg);
+        const int n = cfg->tile_size, N = n * cfg->upsample;
+        if (x0 < 0 || y0 < 0 || y0 + n > height || x0 + n > width) throw DataError("tile extends past frame bounds");
+        cudaStream_t s = ctx->stream;
+        DevBuf<uint16_t> fr;
+        DevBuf<float2> cv;
+        DevBuf<int2> xy;
+        fr.ensure(size_t(height) * width);
+        ck(cudaMemcpy2DAsync(fr.p, size_t(width) * 2, frame, size_t(row_pitch) * 2, size_t(width) * 2, size_t(height),
+                             cudaMemcpyHostToDevice, s), "frame H2D");
+        const int2 o = make_int2(x0, y0);
+        xy.upload(&o, 1, s);
+        cv.ensure(size_t(N) * N);
+        fpmk::LinesArgs la{};
+        la.tw = ctx->twiddle_table(N);
+        la.frame = fr.p;
+        la.pitch = width;
+        la.tile_xy = xy.p;
+        la.n = n;
+        la.up = cfg->upsample;
+        la.src = cv.p;
+        la.dst = cv.p;
+        la.scale = 1.0f;
+        ck(fpmk::launch_lines(0, N, la, 1, s), "init rows");
+        la.scale = float(1.0 / (double(cfg->upsample) * cfg->upsample));
+        ck(fpmk::launch_lines(1, N, la, 1, s), "init cols");
+        ck(cudaMemcpyAsync(canvas, cv.p, sizeof(float2) * size_t(N) * N, cudaMemcpyDeviceToHost, s), "canvas D2H");
+        ck(cudaStreamSynchronize(s), "init_canvas");
+    });
+}
+
+int fpmgpu_canvas_to_field(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const float* canvas, float* field) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int N = cfg->tile_size * cfg->upsample;
+        cudaStream_t s = ctx->stream;
+        DevBuf<float2> cv;
+        cv.upload(reinterpret_cast<const float2*>(canvas), size_t(N) * N, s);
+        fpmk::LinesArgs la{};
+        la.tw = ctx->twiddle_table(N);
+        la.src = cv.p;
+        la.dst = cv.p;
+        la.scale = 1.0f;
+        ck(fpmk::launch_lines(2, N, la, 1, s), "final rows");
+        la.scale = float(double(cfg->upsample) * cfg->upsample / (double(N) * N));
+        ck(fpmk::launch_lines(3, N, la, 1, s), "final cols");
+        ck(cudaMemcpyAsync(field, cv.p, sizeof(float2) * size_t(N) * N, cudaMemcpyDeviceToHost, s), "field D2H");
+        ck(cudaStreamSynchronize(s), "canvas_to_field");
+    });
+}
+
+int fpmgpu_stitch_mosaic(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const float* tiles, const int* xy,
+                         int num_tiles, float* out, int* rows, int* cols) {
+    (void)ctx;
+    (void)cfg;
+    (void)tiles;
+    (void)xy;
+    (void)num_tiles;
+    (void)out;
+    (void)rows;
+    (void)cols;
+    g_err = "stitch_mosaic device kernel not built yet";
+    return FPMGPU_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

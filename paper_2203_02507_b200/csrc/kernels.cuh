@@ -1,0 +1,50 @@
+// Kernel launch interface shared by capi.cu and kernels.cu.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fpmk {
+
+enum { kModeGS = 0, kModeEPRY = 1 };
+enum { kMeasTMA = 0, kMeasF32 = 1 };
+
+// Per-tile LED loop (K1 fused update + K4 persistent loop). One CTA per tile,
+// G groups of 64 threads; group g runs entry g of each schedule slot.
+struct LoopArgs {
+    float2* canvas;           // [T][N][N] spectrum canvases (in/out)
+    float2* pupils;           // [T][n][n] pupils (in; out for EPRY)
+    const uint8_t* support;   // [n][n] pupil support disk (optics.cpp:59-60)
+    const short2* origins;    // [T][L] sub-aperture origin (r0, c0) = N/2 + (oy, ox) - n/2
+    const int* seq_frame;     // [L] frame index of sequence position
+    const int2* tile_xy;      // [T] (x0, y0) of the LR crop
+    double* residuals;        // [T][iters] pass mean residual (recon.cpp:165)
+    const float* meas_f32;    // kMeasF32: [n][n] intensities (update_step API)
+    const int2* slots;        // G > 1: [num_slots][G] (stage, position), stage < 0 = idle
+    int num_slots;            // G == 1: iters * L (implicit slots)
+    int T, L, iters, N, nslots;
+    float alpha, beta;        // EPRY step sizes
+};
+
+// Line FFTs for init_canvas / canvas_to_field (K2 / K3).
+struct LinesArgs {
+    const float2* src;        // [T][N][N]
+    float2* dst;              // [T][N][N]
+    const float2* tw;         // [N] forward twiddles W_N^m
+    const uint16_t* frame;    // init rows: LR frame base (seed frame), row pitch below
+    long long pitch;          // elements
+    const int2* tile_xy;      // [T]
+    int n, up;
+    float scale;
+};
+
+size_t loop_smem_bytes(int G, int nslots, int L, int iters);
+cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorMap* tmap,
+                          const LoopArgs& a, int T, cudaStream_t s);
+// which: 0 init rows (frame -> canvas), 1 init cols, 2 finalize rows, 3 finalize cols
+cudaError_t launch_lines(int which, int N, const LinesArgs& a, int T, cudaStream_t s);
+cudaError_t launch_build_pupils(float2* pupils, const uint8_t* support, const double* defocus,
+                                int n, int T, double dk, double inv_l2, cudaStream_t s);
+
+}  // namespace fpmk

@@ -1,0 +1,190 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle.
+
+Tolerances (north star, BASELINE.json): reconstructed amplitude and phase
+within relative L2 1e-4 per iteration and 1e-3 after the full iteration
+count. The kernel computes in FP32, the oracle in FP64.
+"""
+import numpy as np
+import pytest
+
+import paper_2203_02507_b200 as fpm
+from tests.helpers import amp_phase_rel, dataset, gpu_cfg, orc_cfg, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+PER_ITER_TOL = 1e-4
+FINAL_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def eng():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return fpm.default_engine(0)
+
+
+def test_init_canvas_and_finalize(orc, eng):
+    cfg = gpu_cfg()
+    fs, ofs, seq, _ = dataset(cfg, seed=2)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    got = fpm.init_canvas(fs, t, cfg, engine=eng).spectrum
+    ref = orc.init_canvas(ofs, orc_cfg(cfg))
+    assert rel_l2(got, ref) < 1e-6
+    back = fpm.canvas_to_field(fpm.SpectrumCanvas(got, cfg), engine=eng)
+    ref_back = orc.canvas_to_field(ref, orc_cfg(cfg))
+    assert rel_l2(back, ref_back) < 1e-6
+    # zero iterations round trip (test_recon.cpp:77-86)
+    expected = orc.upsample_bilinear(np.sqrt(fs.images[fs.find(cfg.center_led)].astype(float)), 4)
+    assert np.abs(np.abs(back) - expected).max() / expected.max() < 1e-5
+
+
+@pytest.mark.parametrize("defocus", [0.0, 9.0])
+def test_update_step_matches_oracle(orc, eng, defocus):
+    cfg = gpu_cfg(led_scan_rows=5, led_scan_cols=5)
+    fs, ofs, seq, _ = dataset(cfg, seed=3)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    canvas = orc.init_canvas(ofs, orc_cfg(cfg))
+    pupil = fpm.build_pupil(cfg, 64, defocus)
+    for led in seq[:6]:
+        I = fs.images[fs.find(led)][:64, :64].astype(np.float64)
+        wv = t.wavevectors[led]
+        gc = fpm.SpectrumCanvas(canvas.astype(np.complex64), cfg)
+        r_gpu = fpm.update_step(gc, I, wv, pupil, engine=eng)
+        r_ref = orc.update_step(canvas, I, wv, pupil.values, orc_cfg(cfg))
+        assert r_gpu == pytest.approx(r_ref, rel=1e-4, abs=1e-9)
+        assert rel_l2(gc.spectrum, canvas) < 1e-5
+
+
+def test_update_step_fixed_point(orc, eng):
+    """test_recon.cpp:96-116 on the device: self-consistent data is a fixed point."""
+    cfg = gpu_cfg()
+    fs, ofs, _, _ = dataset(cfg, seed=3)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    canvas = orc.init_canvas(ofs, orc_cfg(cfg))
+    pupil = fpm.build_pupil(cfg, 64)
+    wv = t.wavevectors[(32, 33)]
+    oy, ox = fpm.spectrum_offset_px(wv, cfg)
+    r0, c0 = 128 + oy - 32, 128 + ox - 32
+    I = np.abs(orc.ifft2(canvas[r0:r0 + 64, c0:c0 + 64] * pupil.values)) ** 2
+    gc = fpm.SpectrumCanvas(canvas.astype(np.complex64), cfg)
+    res = fpm.update_step(gc, I, wv, pupil, engine=eng)
+    assert res <= 1e-10
+    assert np.abs(gc.spectrum - canvas).max() / np.abs(canvas).max() <= 1e-6
+
+
+def test_support_confinement_bit_exact(orc, eng):
+    """test_recon.cpp:118-145: pixels outside every updated disk are untouched."""
+    cfg = gpu_cfg()
+    fs, ofs, seq, _ = dataset(cfg, seed=4)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    init = fpm.init_canvas(fs, t, cfg, engine=eng)
+    gc = fpm.SpectrumCanvas(init.spectrum.copy(), cfg)
+    pupil = fpm.build_pupil(cfg, 64)
+    for led in seq:
+        fpm.update_step(gc, fs.images[fs.find(led)][:64, :64], t.wavevectors[led], pupil, engine=eng)
+    N = 256
+    i, j = np.mgrid[0:N, 0:N]
+    inside = np.zeros((N, N), bool)
+    for oy, ox in gc.updated_offsets:
+        inside |= np.hypot(i - (N // 2 + oy), j - (N // 2 + ox)) <= pupil.radius_px
+    assert np.array_equal(gc.spectrum[~inside], init.spectrum[~inside])
+
+
+@pytest.mark.parametrize("iters", [1, 2, 5])
+def test_gs_per_iteration(orc, eng, iters):
+    """Config 1 geometry (64x64 LR, 15x15 LEDs, GS) per iteration count."""
+    cfg = gpu_cfg(led_scan_rows=15, led_scan_cols=15, tile_overlap=0)
+    fs, ofs, seq, _ = dataset(cfg, seed=1)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    got = fpm.reconstruct_tile(fs, t, cfg, iters, seq, engine=eng)
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), iters, seq)
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
+    assert np.allclose(got.metrics.pass_mean_residual, ref.residuals, rtol=1e-3)
+
+
+def test_config1_full_gs(orc, eng):
+    """BASELINE config 1: single 64x64 tile, 15x15 LEDs, 10 iterations GS."""
+    cfg = gpu_cfg(led_scan_rows=15, led_scan_cols=15, tile_overlap=0)
+    fs, ofs, seq, _ = dataset(cfg, seed=1)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    got = fpm.reconstruct_tile(fs, t, cfg, 10, seq, engine=eng)
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), 10, seq)
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < FINAL_TOL and ph < FINAL_TOL, (amp, ph)
+    assert got.metrics.pass_mean_residual[-1] <= got.metrics.pass_mean_residual[0]
+
+
+@pytest.mark.parametrize("iters", [1, 3])
+def test_epry_per_iteration(orc, eng, iters):
+    cfg = gpu_cfg(led_scan_rows=9, led_scan_cols=9, tile_overlap=0)
+    fs, ofs, seq, _ = dataset(cfg, seed=5, defocus_um=25.0)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    got = fpm.reconstruct_tile(fs, t, cfg, iters, seq, mode="epry", engine=eng)
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), iters, seq, mode="epry")
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
+    assert rel_l2(got.pupil, ref.pupil) < PER_ITER_TOL
+
+
+def test_epry_defocused_tile_final(orc, eng):
+    cfg = gpu_cfg(led_scan_rows=15, led_scan_cols=15, tile_overlap=0)
+    fs, ofs, seq, _ = dataset(cfg, seed=6, defocus_um=20.0)
+    tiles = fpm.partition_tiles(64, 64, cfg)
+    tiles[0].defocus_um = 5.0
+    got = fpm.reconstruct_tile(fs, tiles[0], cfg, 10, seq, mode="epry", engine=eng)
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), 10, seq, mode="epry", tile_defocus=5.0)
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < FINAL_TOL and ph < FINAL_TOL, (amp, ph)
+
+
+def test_pipelined_bit_identical_to_sequential(eng):
+    """Spectrum-domain level: pipelined == sequential bit for bit (test_parallel.cpp:79-122)."""
+    cfg = gpu_cfg(led_scan_rows=7, led_scan_cols=7, tile_overlap=0)
+    fs, _, _, _ = dataset(cfg, seed=23)
+    seq = fpm.led_sequence("raster", cfg)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    lag = fpm.min_safe_lag_tile(seq, t, cfg)
+    assert lag < len(seq)
+    a = fpm.reconstruct_tile(fs, t, cfg, 3, seq, engine=eng)
+    b = fpm.pipelined_reconstruct_tile(fs, t, cfg, 3, seq, lag=lag, engine=eng)
+    assert b.lag == lag and not b.nondeterministic
+    assert np.array_equal(a.hr, b.hr)
+    c = fpm.pipelined_reconstruct_tile(fs, t, cfg, 3, seq, engine=eng)
+    assert np.array_equal(a.hr, c.hr)
+
+
+def test_unsafe_lag_refused(eng):
+    cfg = gpu_cfg()
+    fs, _, seq, _ = dataset(cfg, seed=24)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    with pytest.raises(fpm.UnsafeLagError) as ei:
+        fpm.pipelined_reconstruct_tile(fs, t, cfg, 2, seq, lag=1, engine=eng)
+    assert ei.value.minimum == 9
+    f = fpm.pipelined_reconstruct_tile(fs, t, cfg, 2, seq, lag=1, force_unsafe=True, engine=eng)
+    assert f.nondeterministic and np.all(np.isfinite(f.hr))
+
+
+def test_multi_tile_batch_matches_oracle(orc, eng):
+    """Spatial level: many tiles per launch, per-tile k-vectors and defocus pupils (config 3 shape, small FOV)."""
+    cfg = gpu_cfg(led_scan_rows=7, led_scan_cols=7, tile_overlap=8)
+    fs, ofs, seq, _ = dataset(cfg, fov=120, seed=31)
+    rng = np.random.default_rng(7)
+    defocus = rng.uniform(-10, 10, 4)
+    opt = fpm.RunOptions(iters=3, mode="epry", tile_defocus_um=list(defocus))
+    got = fpm.run_offline(fs, cfg, seq, opt, engine=eng, stitch=False)
+    ref = orc.run_offline(ofs, orc_cfg(cfg), seq, 3, mode="epry", tile_defocus=defocus, want_stitched=False)
+    assert got.tiles.shape == ref.tiles.shape == (4, 256, 256)
+    for i in range(4):
+        amp, ph = amp_phase_rel(got.tiles[i], ref.tiles[i])
+        assert amp < FINAL_TOL and ph < FINAL_TOL, (i, amp, ph)
+
+
+def test_offset_out_of_canvas_is_data_error(eng):
+    cfg = gpu_cfg()
+    fs, _, seq, _ = dataset(cfg, seed=2)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    canvas = fpm.init_canvas(fs, t, cfg, engine=eng)
+    with pytest.raises(fpm.DataError, match="spectrum offset out of canvas bounds"):
+        fpm.update_step(canvas, np.ones((64, 64)), (0.95 / cfg.wavelength, 0.0), fpm.build_pupil(cfg, 64),
+                        engine=eng)
