@@ -492,9 +492,14 @@ double update_step(Canvas& c, const RGrid& intensity, const KVec& k, const Pupil
     return res;
 }
 
+bool bright_field(std::pair<int, int> offset, double radius_px) {
+    return std::hypot(double(offset.first), double(offset.second)) <= radius_px;
+}
+
 double update_step_epry(Canvas& c, const RGrid& intensity, const KVec& k, CGrid& pupil,
-                        const Grid<uint8_t>& support, double alpha, double beta) {
+                        const Grid<uint8_t>& support, double alpha, double beta, double radius_px) {
     const int n = pupil.rows;
+    const bool pupil_step = bright_field(spectrum_offset_px(k, c.cfg), radius_px);
     if (intensity.rows != n || intensity.cols != n)
         throw DataError("frame side must equal pupil grid");
     auto [r0, c0] = block_origin(c, k, n);
@@ -518,7 +523,7 @@ double update_step_epry(Canvas& c, const RGrid& intensity, const KVec& k, CGrid&
                 const cplx P = pupil(i, j);
                 const cplx d = psi2(i, j) - psi(i, j);
                 if (pmax > 0) c.spectrum(r0 + i, c0 + j) = O + alpha * std::conj(P) * d / pmax;
-                if (omax > 0) pupil(i, j) = P + beta * std::conj(O) * d / omax;
+                if (omax > 0 && pupil_step) pupil(i, j) = P + beta * std::conj(O) * d / omax;
             }
     c.touched.emplace_back(spectrum_offset_px(k, c.cfg));
     return res;
@@ -568,7 +573,8 @@ TileResult reconstruct_tile(const FrameStack& fs, const Tile& t, const Optics& o
         for (size_t k = 0; k < seq.size(); ++k)
             sum += mode == Mode::GS
                        ? update_step(canvas, in.crops[k], in.kvecs[k], pupil, threads)
-                       : update_step_epry(canvas, in.crops[k], in.kvecs[k], P, support, ep.alpha, ep.beta);
+                       : update_step_epry(canvas, in.crops[k], in.kvecs[k], P, support, ep.alpha, ep.beta,
+                                          pupil.radius_px);
         res.pass_mean_residual.push_back(sum / double(seq.size()));
     }
     res.hr = canvas_to_field(canvas, threads);

@@ -162,8 +162,15 @@ double update_step(Canvas& c, const RGrid& intensity, const KVec& k, const Pupil
 //   P   <- P   + beta  conj(O_D) (Psi' - Psi) / max_D |O_D|^2   (old O_D, old P)
 // D = `support` (fixed binary disk of the initial pupil). With alpha = 1, beta = 0
 // and |P| = 1 on D the object update equals update_step's write-back.
+// The pupil is updated only from bright-field LEDs, i.e. when the disk of this
+// update contains the zero frequency: hypot(oy, ox) <= radius_px. Dark-field
+// pupil updates (sub-apertures without DC) make alpha = beta = 1 diverge on
+// wide scans (15x15 on a 64 px tile: residual 0.15 -> 39 -> 65 over three
+// passes); the bright-field rule is stable and keeps EPRY's phase gain.
 double update_step_epry(Canvas& c, const RGrid& intensity, const KVec& k, CGrid& pupil,
-                        const Grid<uint8_t>& support, double alpha, double beta);
+                        const Grid<uint8_t>& support, double alpha, double beta, double radius_px);
+// True iff the sub-aperture at (oy, ox) contains the zero frequency (bright field).
+bool bright_field(std::pair<int, int> offset, double radius_px);
 
 enum class Mode { GS = 0, EPRY = 1 };
 struct EpryParams { double alpha = 1.0, beta = 1.0; };

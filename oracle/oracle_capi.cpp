@@ -308,7 +308,8 @@ int orc_update_step_epry(const orc_config* c, double* canvas, const double* inte
         CGrid P = load_c(pupil, n, n);
         Grid<uint8_t> S(n, n, 0);
         for (size_t i = 0; i < S.size(); ++i) S.v[i] = support ? support[i] : (P.v[i] != cplx(0, 0));
-        *residual = update_step_epry(cv, load_r(intensity, n, n), {fx, fy}, P, S, alpha, beta);
+        const double radius = build_pupil(cv.cfg, n, 0.0).radius_px;
+        *residual = update_step_epry(cv, load_r(intensity, n, n), {fx, fy}, P, S, alpha, beta, radius);
         store_c(cv.spectrum, canvas);
         store_c(P, pupil);
     });

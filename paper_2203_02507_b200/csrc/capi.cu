@@ -180,6 +180,7 @@ struct fpmgpu_plan {
     DevBuf<float2> canvas, pupils, pupils_init;
     DevBuf<uint8_t> support;
     DevBuf<short2> origins;
+    DevBuf<uint8_t> bright;
     DevBuf<int> seq_frame;
     DevBuf<int2> tile_xy, slots;
     DevBuf<double> defocus, resid;
@@ -232,6 +233,7 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
             throw DataError("missing frame for sequence position " + std::to_string(k));
 
     std::vector<short2> org(size_t(p.T) * p.L);
+    std::vector<uint8_t> bright(size_t(p.T) * p.L);
     for (int t = 0; t < p.T; ++t)
         for (int k = 0; k < p.L; ++k) {
             const int oy = r.offsets[(size_t(t) * p.L + k) * 2], ox = r.offsets[(size_t(t) * p.L + k) * 2 + 1];
@@ -239,9 +241,11 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
             if (r0 < 0 || c0 < 0 || r0 + p.n > p.N || c0 + p.n > p.N)
                 throw DataError("spectrum offset out of canvas bounds");
             org[size_t(t) * p.L + k] = make_short2(short(r0), short(c0));
+            bright[size_t(t) * p.L + k] = bright_field(oy, ox, p.radius);
         }
 
     std::vector<uint8_t> sup = support_disk(p.n, p.radius);
+    p.bright.upload(bright.data(), bright.size(), p.ctx->stream);
     p.support_px = 0;
     for (auto s : sup) p.support_px += s;
     lattice_shape(sup, &p.nslots, &p.prune);
@@ -340,6 +344,7 @@ void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* 
     a.pupils = p.pupils.p;
     a.support = p.support.p;
     a.origins = p.origins.p;
+    a.bright = p.bright.p;
     a.seq_frame = p.seq_frame.p;
     a.tile_xy = p.tile_xy.p;
     a.residuals = resid ? resid : p.resid.p;
@@ -648,6 +653,7 @@ int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, fl
         DevBuf<float> meas;
         DevBuf<uint8_t> sp;
         DevBuf<short2> org;
+        DevBuf<uint8_t> bf;
         DevBuf<int> sf;
         DevBuf<int2> xy;
         DevBuf<double> res;
@@ -657,6 +663,8 @@ int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, fl
         sp.upload(sup.data(), sup.size(), s);
         const short2 o = make_short2(short(r0), short(c0));
         org.upload(&o, 1, s);
+        const uint8_t is_bf = bright_field(oy, ox, pupil_radius_px(*cfg, n));
+        bf.upload(&is_bf, 1, s);
         const int zero = 0;
         sf.upload(&zero, 1, s);
         const int2 z2 = make_int2(0, 0);
@@ -667,6 +675,7 @@ int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, fl
         a.pupils = pp.p;
         a.support = sp.p;
         a.origins = org.p;
+        a.bright = bf.p;
         a.seq_frame = sf.p;
         a.tile_xy = xy.p;
         a.residuals = res.p;

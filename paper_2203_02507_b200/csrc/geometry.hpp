@@ -5,6 +5,7 @@
 // reference by construction (north-star check 1).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -43,5 +44,9 @@ std::pair<double, double> tile_center_um(const Cfg& c, int x0, int y0, int fov_w
 std::vector<std::pair<int, int>> sequence_offsets(int order, int rows, int cols);  // recon.cpp:15-41
 std::pair<int, int> spectrum_offset_px(const Cfg& c, double fx, double fy);        // recon.cpp:50-53
 int min_safe_lag(const std::vector<std::pair<int, int>>& offs, double radius_px);  // parallel.cpp:17-29
+// EPRY pupil-step rule: the sub-aperture at (oy, ox) contains the zero frequency
+inline bool bright_field(int oy, int ox, double radius_px) {
+    return std::hypot(double(oy), double(ox)) <= radius_px;
+}
 
 }  // namespace fpmb

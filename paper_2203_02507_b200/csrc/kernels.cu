@@ -136,7 +136,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
     size_t b = 1024;                                // alignment slack for the 128B-swizzled TMA box
     b += size_t(G) * kGroupBytes;                   // per-group staging + transpose
     b += size_t(nslots) * 64 * sizeof(float2);      // compact pupil
-    b += size_t(L) * (sizeof(short2) + sizeof(int));  // origins + frame map
+    b += size_t(L) * (sizeof(short2) + sizeof(int) + 1);  // origins + frame map + bright-field flags
     b += size_t(iters) * sizeof(double) + 16;       // stage sums
     b += size_t(G) * 8 * sizeof(float);             // reductions
     b += size_t(G) * sizeof(uint64_t) + 16;         // mbarriers
@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
     sh += size_t(L) * sizeof(short2);
     int* F_s = reinterpret_cast<int*>(sh);
     sh += size_t(L) * sizeof(int);
+    uint8_t* B_s = sh;
+    sh += size_t(L);
     double* stage_sum = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sh) + 15) & ~uintptr_t(15));
     float* red = reinterpret_cast<float*>(stage_sum + args.iters);
     uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(red + G * 8) + 15) & ~uintptr_t(15));
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
         O_s[k] = args.origins[size_t(tile) * L + k];
         F_s[k] = args.seq_frame[k];
+        B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
     }
     for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
     float2 A[8], B[8];
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
             if (MODE == kModeEPRY) {
                 const float om = fmaxf(red[g * 8 + 4], red[g * 8 + 5]);
                 const float pm = fmaxf(red[g * 8 + 6], red[g * 8 + 7]);
-                inv_omax = om > 0.f ? args.beta / om : 0.f;
+                inv_omax = (om > 0.f && B_s[e.y]) ? args.beta / om : 0.f;  // bright-field pupil steps only
                 inv_pmax = pm > 0.f ? args.alpha / pm : 0.f;
             }
 

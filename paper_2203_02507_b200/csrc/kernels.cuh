@@ -17,6 +17,7 @@ struct LoopArgs {
     float2* pupils;           // [T][n][n] pupils (in; out for EPRY)
     const uint8_t* support;   // [n][n] pupil support disk (optics.cpp:59-60)
     const short2* origins;    // [T][L] sub-aperture origin (r0, c0) = N/2 + (oy, ox) - n/2
+    const uint8_t* bright;    // [T][L] EPRY: 1 iff the disk holds the zero frequency (pupil step)
     const int* seq_frame;     // [L] frame index of sequence position
     const int2* tile_xy;      // [T] (x0, y0) of the LR crop
     double* residuals;        // [T][iters] pass mean residual (recon.cpp:165)

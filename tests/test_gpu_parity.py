@@ -112,7 +112,7 @@ def test_config1_full_gs(orc, eng):
     ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), 10, seq)
     amp, ph = amp_phase_rel(got.hr, ref.hr)
     assert amp < FINAL_TOL and ph < FINAL_TOL, (amp, ph)
-    assert got.metrics.pass_mean_residual[-1] <= got.metrics.pass_mean_residual[0]
+    assert np.allclose(got.metrics.pass_mean_residual, ref.residuals, rtol=1e-3)
 
 
 @pytest.mark.parametrize("iters", [1, 3])
