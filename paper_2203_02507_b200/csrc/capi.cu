@@ -130,8 +130,9 @@ void lattice_shape(const std::vector<uint8_t>& support, int* nslots, bool* prune
             }
         mx = std::max(mx, c);
     }
-    *nslots = std::max(mx, 1);
+    (void)mx;
     *prune = inside;
+    *nslots = inside ? 16 : 64;  // lattice positions per thread held in the shared pupil
 }
 
 std::vector<float2> twiddles(int N) {
@@ -249,6 +250,8 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     p.support_px = 0;
     for (auto s : sup) p.support_px += s;
     lattice_shape(sup, &p.nslots, &p.prune);
+    if (!p.prune && p.N != 256)
+        throw Unsupported("pupil disk wider than the pruned lattice needs canvas side 256 in this build");
 
     // pipelined schedule (parallel.cpp:52-111): one lag for the whole batch,
     // the largest per-tile minimum, so every tile stays sequential-equivalent
@@ -648,6 +651,9 @@ int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, fl
         int nslots;
         bool prune;
         lattice_shape(sup, &nslots, &prune);
+        if (N != 256 && N != 512 && N != 1024) throw Unsupported("canvas side " + std::to_string(N) + " unsupported");
+        if (!prune && N != 256)
+            throw Unsupported("pupil disk wider than the pruned lattice needs canvas side 256 in this build");
         cudaStream_t s = ctx->stream;
         DevBuf<float2> cv, pp;
         DevBuf<float> meas;

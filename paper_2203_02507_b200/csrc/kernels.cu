@@ -27,7 +27,8 @@ namespace fpmk {
 namespace {
 
 constexpr int kIBytes = 64 * 64 * 2;        // staged u16 measurement, TMA 128B-swizzled
-constexpr int kTBytes = 64 * 64 * 8;        // transpose buffer
+constexpr int kTStride = 65;               // transpose row stride (float2): conflict-free both ways
+constexpr int kTBytes = ((64 * kTStride * 8 + 1023) / 1024) * 1024;  // transpose buffer
 constexpr int kGroupBytes = kIBytes + kTBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -72,16 +73,22 @@ __device__ __forceinline__ void group_sync(int g) {
     asm volatile("bar.sync %0, 64;" ::"r"(g + 1) : "memory");
 }
 
+// Cooley-Tukey twiddle W64^(n0r k0r + n0c k0c) of the lattice block, from the
+// shared W64 table (forward sign; INV uses the conjugate).
 template <bool INV>
-__device__ __forceinline__ void twiddle64(float2 (&v)[8][8], const float2 (&A)[8], const float2 (&B)[8]) {
+__device__ __forceinline__ void twiddle64(float2 (&v)[8][8], const float2* W_s, int tr, int tc) {
 #pragma unroll
-    for (int k1 = 1; k1 < 8; ++k1)
+    for (int k1 = 1; k1 < 8; ++k1) {
+        const float2 w = W_s[(tr * k1) & 63];
 #pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) v[k1][k2] = INV ? cmulc(v[k1][k2], A[k1]) : cmul(v[k1][k2], A[k1]);
+        for (int k2 = 0; k2 < 8; ++k2) v[k1][k2] = INV ? cmulc(v[k1][k2], w) : cmul(v[k1][k2], w);
+    }
 #pragma unroll
-    for (int k2 = 1; k2 < 8; ++k2)
+    for (int k2 = 1; k2 < 8; ++k2) {
+        const float2 w = W_s[(tc * k2) & 63];
 #pragma unroll
-        for (int k1 = 0; k1 < 8; ++k1) v[k1][k2] = INV ? cmulc(v[k1][k2], B[k2]) : cmul(v[k1][k2], B[k2]);
+        for (int k1 = 0; k1 < 8; ++k1) v[k1][k2] = INV ? cmulc(v[k1][k2], w) : cmul(v[k1][k2], w);
+    }
 }
 
 // Step 2 of a 64x64 transform: 2-D 8x8 DFT over the transposed block.
@@ -102,16 +109,15 @@ __device__ __forceinline__ void dft8x8_out(float2 (&v)[8][8]) {
 // Full 64x64 centered-core transform on the lattice block (without the
 // checkerboard signs, which the caller folds into gather/scatter).
 template <bool INV, bool PRUNE_IN, bool PRUNE_OUT>
-__device__ __forceinline__ void fft64x64(float2 (&v)[8][8], float2* T_s, int t, int g,
-                                         const float2 (&A)[8], const float2 (&B)[8]) {
+__device__ __forceinline__ void fft64x64(float2 (&v)[8][8], float2* T_s, const float2* W_s, int t, int g) {
     dft8x8<INV, PRUNE_IN>(v);
-    twiddle64<INV>(v, A, B);
+    twiddle64<INV>(v, W_s, t >> 3, t & 7);
 #pragma unroll
     for (int k1 = 0; k1 < 8; ++k1)
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
             const int d = k1 * 8 + k2;
-            T_s[d * 64 + (t ^ (d & 15))] = v[k1][k2];
+            T_s[d * kTStride + t] = v[k1][k2];
         }
     group_sync(g);
 #pragma unroll
@@ -119,7 +125,7 @@ __device__ __forceinline__ void fft64x64(float2 (&v)[8][8], float2* T_s, int t, 
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
             const int s = a * 8 + b;
-            v[a][b] = T_s[t * 64 + (s ^ (t & 15))];
+            v[a][b] = T_s[t * kTStride + s];
         }
     dft8x8_out<INV, PRUNE_OUT>(v);
 }
@@ -133,61 +139,72 @@ __device__ __forceinline__ int2 slot_entry(const LoopArgs& a, int s, int g) {
 }  // namespace
 
 size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
-    size_t b = 1024;                                // alignment slack for the 128B-swizzled TMA box
-    b += size_t(G) * kGroupBytes;                   // per-group staging + transpose
-    b += size_t(nslots) * 64 * sizeof(float2);      // compact pupil
-    b += size_t(L) * (sizeof(short2) + sizeof(int) + 1);  // origins + frame map + bright-field flags
-    b += size_t(iters) * sizeof(double) + 16;       // stage sums
-    b += size_t(G) * 8 * sizeof(float);             // reductions
-    b += size_t(G) * sizeof(uint64_t) + 16;         // mbarriers
+    size_t b = 1024;                                  // alignment slack for the 128B-swizzled TMA box
+    b += size_t(G) * kGroupBytes;                     // per-group staging + transpose
+    b += size_t(nslots) * 64 * sizeof(float2);        // lattice pupil [NP][64]
+    b += 64 * sizeof(float2);                         // W64 table
+    b += size_t(iters) * sizeof(double);              // stage sums
+    b += size_t(G) * (sizeof(uint64_t) + 8 * sizeof(float));  // mbarriers + reductions
+    b += size_t(L) * (sizeof(short2) + sizeof(int) + 1);      // origins + frame map + bright-field flags
     return b;
 }
 
-template <int MODE, bool PRUNE, int MEAS, int G>
+// Lattice positions a thread may own inside the pupil support: with PRUNE the
+// disk lies in rows/cols [16, 48), i.e. a, b in [2, 6) (16 positions);
+// otherwise all 64.
+template <bool PRUNE>
+struct Lattice {
+    static constexpr int NP = PRUNE ? 16 : 64;
+    __device__ static constexpr int a(int q) { return PRUNE ? 2 + (q >> 2) : (q >> 3); }
+    __device__ static constexpr int b(int q) { return PRUNE ? 2 + (q & 3) : (q & 7); }
+};
+
+template <int MODE, bool PRUNE, int MEAS, int G, int N>
 __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUtensorMap tmap, const LoopArgs args) {
+    using Lat = Lattice<PRUNE>;
+    constexpr int NP = Lat::NP;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align inside the shared window by offset so every pointer keeps the shared state space
+    const uint32_t base = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((base + 1023u) & ~1023u) - base);
     const int g = threadIdx.x >> 6;
     const int t = threadIdx.x & 63;
     const int tr = t >> 3, tc = t & 7;
     const int tile = blockIdx.x;
-    const int N = args.N, L = args.L;
+    const int L = args.L;
 
     uint16_t* I_s = reinterpret_cast<uint16_t*>(smem + g * kGroupBytes);
     float2* T_s = reinterpret_cast<float2*>(smem + g * kGroupBytes + kIBytes);
-    uint8_t* sh = smem + G * kGroupBytes;
-    float2* P_s = reinterpret_cast<float2*>(sh);
-    sh += size_t(args.nslots) * 64 * sizeof(float2);
-    short2* O_s = reinterpret_cast<short2*>(sh);
-    sh += size_t(L) * sizeof(short2);
-    int* F_s = reinterpret_cast<int*>(sh);
-    sh += size_t(L) * sizeof(int);
-    uint8_t* B_s = sh;
-    sh += size_t(L);
-    double* stage_sum = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sh) + 15) & ~uintptr_t(15));
-    float* red = reinterpret_cast<float*>(stage_sum + args.iters);
-    uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(red + G * 8) + 15) & ~uintptr_t(15));
+    size_t off = size_t(G) * kGroupBytes;
+    float2* P_s = reinterpret_cast<float2*>(smem + off);  // [NP][64], zero off the support
+    off += size_t(NP) * 64 * sizeof(float2);
+    float2* W_s = reinterpret_cast<float2*>(smem + off);  // W64^m, m in [0, 64)
+    off += 64 * sizeof(float2);
+    double* stage_sum = reinterpret_cast<double*>(smem + off);
+    off += size_t(args.iters) * sizeof(double);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off);
+    off += size_t(G) * sizeof(uint64_t);
+    float* red = reinterpret_cast<float*>(smem + off);
+    off += size_t(G) * 8 * sizeof(float);
+    short2* O_s = reinterpret_cast<short2*>(smem + off);
+    off += size_t(L) * sizeof(short2);
+    int* F_s = reinterpret_cast<int*>(smem + off);
+    off += size_t(L) * sizeof(int);
+    uint8_t* B_s = smem + off;
     uint64_t* bar = bars + g;
 
     float2* canvas = args.canvas + size_t(tile) * N * N;
     float2* pupil_g = args.pupils + size_t(tile) * 64 * 64;
     const int2 txy = args.tile_xy[tile];
 
-    // ---- one-time setup: support mask, compact pupil, tables, twiddles
+    // ---- one-time setup: support mask, lattice pupil, tables, twiddle table
     uint64_t mask = 0;
-    {
-        int slot = 0;
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const int i = tr + 8 * a, j = tc + 8 * b;
-                if (args.support[i * 64 + j]) {
-                    mask |= 1ull << (a * 8 + b);
-                    if (g == 0) P_s[slot * 64 + t] = pupil_g[i * 64 + j];
-                    ++slot;
-                }
-            }
+    for (int q = 0; q < NP; ++q) {
+        const int i = tr + 8 * Lat::a(q), j = tc + 8 * Lat::b(q);
+        const bool on = args.support[i * 64 + j] != 0;
+        mask |= uint64_t(on) << q;
+        if (g == 0) P_s[q * 64 + t] = on ? pupil_g[i * 64 + j] : make_float2(0.f, 0.f);
     }
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
         O_s[k] = args.origins[size_t(tile) * L + k];
@@ -195,14 +212,10 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
         B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
     }
     for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
-    float2 A[8], B[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    if (threadIdx.x < 64) {
         double s, c;
-        sincospi(-double(tr * k) / 32.0, &s, &c);
-        A[k] = make_float2(float(c), float(s));
-        sincospi(-double(tc * k) / 32.0, &s, &c);
-        B[k] = make_float2(float(c), float(s));
+        sincospi(-double(threadIdx.x) / 32.0, &s, &c);
+        W_s[threadIdx.x] = make_float2(float(c), float(s));
     }
     if (MEAS == kMeasTMA && t == 0) {
         mbar_init(bar, 1);
@@ -230,34 +243,31 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
             const short2 o = O_s[e.y];
             float2* cv = canvas + size_t(o.x) * N + o.y;
 
-            // ---- gather the pupil disk of the sub-aperture, times P and the checkerboard
+            // ---- gather: all disk loads in flight at once (every lattice address lies in
+            // the n x n block, so the loads need no predicate), then times P and the sign
             float2 v[8][8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) v[a][b] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < NP; ++q) v[Lat::a(q)][Lat::b(q)] = cv[(tr + 8 * Lat::a(q)) * N + tc + 8 * Lat::b(q)];
             float omax = 0.f, pmax = 0.f;
-            {
-                int slot = 0;
 #pragma unroll
-                for (int a = 0; a < 8; ++a)
-#pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        v[a][b] = make_float2(0.f, 0.f);
-                        if (PRUNE && (a < 2 || a > 5 || b < 2 || b > 5)) continue;
-                        if ((mask >> (a * 8 + b)) & 1ull) {
-                            const float2 O = cv[(tr + 8 * a) * N + tc + 8 * b];
-                            const float2 P = P_s[slot * 64 + t];
-                            ++slot;
-                            v[a][b] = cscale(cmul(O, P), sgn);
-                            if (MODE == kModeEPRY) {
-                                omax = fmaxf(omax, cabs2(O));
-                                pmax = fmaxf(pmax, cabs2(P));
-                            }
-                        }
-                    }
+            for (int q = 0; q < NP; ++q) {
+                const float2 O = v[Lat::a(q)][Lat::b(q)];
+                const float2 P = P_s[q * 64 + t];
+                if (MODE == kModeEPRY) {
+                    omax = fmaxf(omax, ((mask >> q) & 1ull) ? cabs2(O) : 0.f);
+                    pmax = fmaxf(pmax, cabs2(P));
+                }
+                v[Lat::a(q)][Lat::b(q)] = cscale(cmul(O, P), sgn);
             }
             if (MODE == kModeEPRY) {
 #pragma unroll
-                for (int off = 16; off; off >>= 1) {
-                    omax = fmaxf(omax, __shfl_xor_sync(0xffffffffu, omax, off));
-                    pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, off));
+                for (int sh = 16; sh; sh >>= 1) {
+                    omax = fmaxf(omax, __shfl_xor_sync(0xffffffffu, omax, sh));
+                    pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, sh));
                 }
                 if ((t & 31) == 0) {
                     red[g * 8 + 4 + (t >> 5)] = omax;
@@ -266,7 +276,7 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
             }
 
             // ---- centered inverse transform (unscaled; 1/n^2 enters only the residual)
-            fft64x64<true, PRUNE, false>(v, T_s, t, g, A, B);
+            fft64x64<true, PRUNE, false>(v, T_s, W_s, t, g);
 
             // ---- modulus replacement with sqrt(I) and residual sums (recon.cpp:115-124)
             if (MEAS == kMeasTMA) {
@@ -288,21 +298,18 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
                     const float meas = Iv > 0.f ? Iv * rsqrtf(Iv) : 0.f;
                     const float2 u = v[a][b];
                     const float m2 = cabs2(u);
-                    if (m2 > 0.f) {
-                        const float r = rsqrtf(m2);
-                        const float d = fmaf(m2 * r, inv_n2, -meas);
-                        num = fmaf(d, d, num);
-                        v[a][b] = cscale(u, meas * r);
-                    } else {
-                        num = fmaf(meas, meas, num);
-                        v[a][b] = make_float2(sgn * meas, 0.f);
-                    }
+                    const float r = rsqrtf(m2);
+                    const bool nz = m2 > 0.f;
+                    const float dm = nz ? fmaf(m2 * r, inv_n2, -meas) : -meas;
+                    num = fmaf(dm, dm, num);
+                    const float sc = meas * r;
+                    v[a][b] = nz ? cscale(u, sc) : make_float2(sgn * meas, 0.f);
                     den += Iv;
                 }
 #pragma unroll
-            for (int off = 16; off; off >>= 1) {
-                num += __shfl_xor_sync(0xffffffffu, num, off);
-                den += __shfl_xor_sync(0xffffffffu, den, off);
+            for (int sh = 16; sh; sh >>= 1) {
+                num += __shfl_xor_sync(0xffffffffu, num, sh);
+                den += __shfl_xor_sync(0xffffffffu, den, sh);
             }
             if ((t & 31) == 0) {
                 red[g * 8 + (t >> 5)] = num;
@@ -332,31 +339,35 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
             }
 
             // ---- centered forward transform of the corrected field
-            fft64x64<false, false, PRUNE>(v, T_s, t, g, A, B);
+            fft64x64<false, false, PRUNE>(v, T_s, W_s, t, g);
 
             // ---- scatter into the canvas disk (recon.cpp:127-130) / EPRY update
-            {
-                int slot = 0;
+            if (MODE == kModeGS) {
 #pragma unroll
-                for (int a = 0; a < 8; ++a)
+                for (int q = 0; q < NP; ++q)
+                    if ((mask >> q) & 1ull)
+                        cv[(tr + 8 * Lat::a(q)) * N + tc + 8 * Lat::b(q)] =
+                            cmulc(cscale(v[Lat::a(q)][Lat::b(q)], sgn), P_s[q * 64 + t]);
+            } else {
+                const bool upd_o = inv_pmax > 0.f, upd_p = inv_omax > 0.f;
 #pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        if (PRUNE && (a < 2 || a > 5 || b < 2 || b > 5)) continue;
-                        if ((mask >> (a * 8 + b)) & 1ull) {
-                            float2* dst = cv + (tr + 8 * a) * N + tc + 8 * b;
-                            const float2 psi2 = cscale(v[a][b], sgn);
-                            const float2 P = P_s[slot * 64 + t];
-                            if (MODE == kModeGS) {
-                                *dst = cmulc(psi2, P);
-                            } else {
-                                const float2 O = *dst;
-                                const float2 d = csub(psi2, cmul(O, P));
-                                if (inv_pmax > 0.f) *dst = cadd(O, cscale(cmulc(d, P), inv_pmax));
-                                if (inv_omax > 0.f) P_s[slot * 64 + t] = cadd(P, cscale(cmulc(d, O), inv_omax));
-                            }
-                            ++slot;
-                        }
+                for (int c0 = 0; c0 < NP; c0 += 16) {
+                    float2 Ov[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        Ov[q] = cv[(tr + 8 * Lat::a(c0 + q)) * N + tc + 8 * Lat::b(c0 + q)];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const int qq = c0 + q;
+                        const bool on = (mask >> qq) & 1ull;
+                        const float2 O = Ov[q];
+                        const float2 P = P_s[qq * 64 + t];
+                        const float2 d = csub(cscale(v[Lat::a(qq)][Lat::b(qq)], sgn), cmul(O, P));
+                        if (on && upd_o)
+                            cv[(tr + 8 * Lat::a(qq)) * N + tc + 8 * Lat::b(qq)] = cadd(O, cscale(cmulc(d, P), inv_pmax));
+                        if (on && upd_p) P_s[qq * 64 + t] = cadd(P, cscale(cmulc(d, O), inv_omax));
                     }
+                }
             }
         }
         __syncthreads();  // round barrier: canvas writes visible to the next update's gather
@@ -366,22 +377,16 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
     for (int k = threadIdx.x; k < args.iters; k += blockDim.x)
         args.residuals[size_t(tile) * args.iters + k] = stage_sum[k] / double(L);
     if (MODE == kModeEPRY && g == 0) {
-        int slot = 0;
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-                if ((mask >> (a * 8 + b)) & 1ull) {
-                    pupil_g[(tr + 8 * a) * 64 + tc + 8 * b] = P_s[slot * 64 + t];
-                    ++slot;
-                }
+        for (int q = 0; q < NP; ++q)
+            if ((mask >> q) & 1ull) pupil_g[(tr + 8 * Lat::a(q)) * 64 + tc + 8 * Lat::b(q)] = P_s[q * 64 + t];
     }
 }
 
-template <int MODE, bool PRUNE, int MEAS, int G>
+template <int MODE, bool PRUNE, int MEAS, int G, int N>
 static cudaError_t launch_loop_t(const CUtensorMap* tmap, const LoopArgs& a, int T, cudaStream_t s) {
     const size_t smem = loop_smem_bytes(G, a.nslots, a.L, a.iters);
-    auto k = fpm_loop64<MODE, PRUNE, MEAS, G>;
+    auto k = fpm_loop64<MODE, PRUNE, MEAS, G, N>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     k<<<T, 64 * G, smem, s>>>(*tmap, a);
@@ -390,19 +395,22 @@ static cudaError_t launch_loop_t(const CUtensorMap* tmap, const LoopArgs& a, int
 
 cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorMap* tmap,
                           const LoopArgs& a, int T, cudaStream_t s) {
-#define FPM_LOOP_CASE(M, P, ME, GG)                                                   \
-    if (mode == M && prune == P && meas == ME && G == GG)                             \
-        return launch_loop_t<M, P, ME, GG>(tmap, a, T, s);
-    FPM_LOOP_CASE(kModeGS, true, kMeasTMA, 1)
-    FPM_LOOP_CASE(kModeGS, false, kMeasTMA, 1)
-    FPM_LOOP_CASE(kModeEPRY, true, kMeasTMA, 1)
-    FPM_LOOP_CASE(kModeEPRY, false, kMeasTMA, 1)
-    FPM_LOOP_CASE(kModeGS, true, kMeasTMA, 2)
-    FPM_LOOP_CASE(kModeGS, false, kMeasTMA, 2)
-    FPM_LOOP_CASE(kModeGS, true, kMeasF32, 1)
-    FPM_LOOP_CASE(kModeGS, false, kMeasF32, 1)
-    FPM_LOOP_CASE(kModeEPRY, true, kMeasF32, 1)
-    FPM_LOOP_CASE(kModeEPRY, false, kMeasF32, 1)
+#define FPM_LOOP_CASE(M, P, ME, GG, NN)                                               \
+    if (mode == M && prune == P && meas == ME && G == GG && a.N == NN)                \
+        return launch_loop_t<M, P, ME, GG, NN>(tmap, a, T, s);
+#define FPM_LOOP_N(M, P, ME, GG) \
+    FPM_LOOP_CASE(M, P, ME, GG, 256) FPM_LOOP_CASE(M, P, ME, GG, 512) FPM_LOOP_CASE(M, P, ME, GG, 1024)
+    FPM_LOOP_N(kModeGS, true, kMeasTMA, 1)
+    FPM_LOOP_N(kModeEPRY, true, kMeasTMA, 1)
+    FPM_LOOP_N(kModeGS, true, kMeasTMA, 2)
+    FPM_LOOP_CASE(kModeGS, false, kMeasTMA, 1, 256)
+    FPM_LOOP_CASE(kModeEPRY, false, kMeasTMA, 1, 256)
+    FPM_LOOP_CASE(kModeGS, false, kMeasTMA, 2, 256)
+    FPM_LOOP_N(kModeGS, true, kMeasF32, 1)
+    FPM_LOOP_N(kModeEPRY, true, kMeasF32, 1)
+    FPM_LOOP_CASE(kModeGS, false, kMeasF32, 1, 256)
+    FPM_LOOP_CASE(kModeEPRY, false, kMeasF32, 1, 256)
+#undef FPM_LOOP_N
 #undef FPM_LOOP_CASE
     return cudaErrorInvalidConfiguration;
 }
