@@ -204,7 +204,8 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
         const int i = tr + 8 * Lat::a(q), j = tc + 8 * Lat::b(q);
         const bool on = args.support[i * 64 + j] != 0;
         mask |= uint64_t(on) << q;
-        if (g == 0) P_s[q * 64 + t] = on ? pupil_g[i * 64 + j] : make_float2(0.f, 0.f);
+        // the shared pupil carries the thread's checkerboard sign: P' = (-1)^(i+j) P
+        if (g == 0) P_s[q * 64 + t] = on ? cscale(pupil_g[i * 64 + j], ((tr + tc) & 1) ? -1.f : 1.f) : make_float2(0.f, 0.f);
     }
     for (int k = threadIdx.x; k < L; k += blockDim.x) {
         O_s[k] = args.origins[size_t(tile) * L + k];
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
                     omax = fmaxf(omax, ((mask >> q) & 1ull) ? cabs2(O) : 0.f);
                     pmax = fmaxf(pmax, cabs2(P));
                 }
-                v[Lat::a(q)][Lat::b(q)] = cscale(cmul(O, P), sgn);
+                v[Lat::a(q)][Lat::b(q)] = cmul(O, P);  // sign folded into P'
             }
             if (MODE == kModeEPRY) {
 #pragma unroll
@@ -283,7 +284,11 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
                 mbar_wait(bar, phase);
                 phase ^= 1u;
             }
-            float num = 0.f, den = 0.f;
+            // e' = e sqrt(I)/|e| (or sqrt(I) + 0i at |e| = 0, recon.cpp:122); the residual is
+            // formed from the difference |e| - sqrt(I) itself so small residuals stay exact
+            // (a one-rsqrt expansion |e|^2 - 2|e|sqrt(I) + I cancels catastrophically).
+            float num = 0.f, den_f = 0.f;
+            uint32_t den_u = 0;
 #pragma unroll
             for (int a = 0; a < 8; ++a)
 #pragma unroll
@@ -291,21 +296,27 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
                     float Iv;
                     if (MEAS == kMeasTMA) {
                         // 128B swizzle: 16-byte chunk b of row i sits at chunk b ^ (i & 7), i & 7 == tr
-                        Iv = float(I_s[(tr + 8 * a) * 64 + ((b ^ tr) << 3) + tc]);
+                        const uint32_t Iu = I_s[(tr + 8 * a) * 64 + ((b ^ tr) << 3) + tc];
+                        den_u += Iu;
+                        Iv = float(Iu);
                     } else {
                         Iv = args.meas_f32[(tr + 8 * a) * 64 + tc + 8 * b];
+                        den_f += Iv;
                     }
                     const float meas = Iv > 0.f ? Iv * rsqrtf(Iv) : 0.f;
                     const float2 u = v[a][b];
                     const float m2 = cabs2(u);
-                    const float r = rsqrtf(m2);
-                    const bool nz = m2 > 0.f;
-                    const float dm = nz ? fmaf(m2 * r, inv_n2, -meas) : -meas;
-                    num = fmaf(dm, dm, num);
-                    const float sc = meas * r;
-                    v[a][b] = nz ? cscale(u, sc) : make_float2(sgn * meas, 0.f);
-                    den += Iv;
+                    if (__builtin_expect(m2 > 0.f, 1)) {
+                        const float r = rsqrtf(m2);
+                        const float dm = fmaf(m2 * r, inv_n2, -meas);
+                        num = fmaf(dm, dm, num);
+                        v[a][b] = cscale(u, meas * r);
+                    } else {
+                        num = fmaf(meas, meas, num);
+                        v[a][b] = make_float2(sgn * meas, 0.f);
+                    }
                 }
+            float den = MEAS == kMeasTMA ? float(den_u) : den_f;
 #pragma unroll
             for (int sh = 16; sh; sh >>= 1) {
                 num += __shfl_xor_sync(0xffffffffu, num, sh);
@@ -346,8 +357,7 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
 #pragma unroll
                 for (int q = 0; q < NP; ++q)
                     if ((mask >> q) & 1ull)
-                        cv[(tr + 8 * Lat::a(q)) * N + tc + 8 * Lat::b(q)] =
-                            cmulc(cscale(v[Lat::a(q)][Lat::b(q)], sgn), P_s[q * 64 + t]);
+                        cv[(tr + 8 * Lat::a(q)) * N + tc + 8 * Lat::b(q)] = cmulc(v[Lat::a(q)][Lat::b(q)], P_s[q * 64 + t]);
             } else {
                 const bool upd_o = inv_pmax > 0.f, upd_p = inv_omax > 0.f;
 #pragma unroll
@@ -362,7 +372,9 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
                         const bool on = (mask >> qq) & 1ull;
                         const float2 O = Ov[q];
                         const float2 P = P_s[qq * 64 + t];
-                        const float2 d = csub(cscale(v[Lat::a(qq)][Lat::b(qq)], sgn), cmul(O, P));
+                        // with P' = sP and Psi' = s v: d' = s d, conj(P') d' = conj(P) d,
+                        // P'_new = P' + beta conj(O) d' / max|O|^2 (s = checkerboard sign)
+                        const float2 d = csub(v[Lat::a(qq)][Lat::b(qq)], cmul(O, P));
                         if (on && upd_o)
                             cv[(tr + 8 * Lat::a(qq)) * N + tc + 8 * Lat::b(qq)] = cadd(O, cscale(cmulc(d, P), inv_pmax));
                         if (on && upd_p) P_s[qq * 64 + t] = cadd(P, cscale(cmulc(d, O), inv_omax));
@@ -379,7 +391,7 @@ __global__ void __launch_bounds__(64 * G) fpm_loop64(const __grid_constant__ CUt
     if (MODE == kModeEPRY && g == 0) {
 #pragma unroll
         for (int q = 0; q < NP; ++q)
-            if ((mask >> q) & 1ull) pupil_g[(tr + 8 * Lat::a(q)) * 64 + tc + 8 * Lat::b(q)] = P_s[q * 64 + t];
+            if ((mask >> q) & 1ull) pupil_g[(tr + 8 * Lat::a(q)) * 64 + tc + 8 * Lat::b(q)] = cscale(P_s[q * 64 + t], sgn);
     }
 }
 
