@@ -172,6 +172,11 @@ int fpmgpu_canvas_to_field(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg
  * origins xy [T][2]; out [rows][cols] complex64 (host) or NULL to query the size. */
 int fpmgpu_stitch_mosaic(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const float* tiles,
                          const int* xy, int num_tiles, float* out, int* rows, int* cols);
+/* Same on device buffers (tiles_dev [T][N][N], out_dev [rows][cols] complex64;
+ * out_dev NULL = size query), enqueued on `stream` (cudaStream_t). */
+int fpmgpu_stitch_mosaic_device(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg,
+                                const float* tiles_dev, const int* xy, int num_tiles, float* out_dev,
+                                int* rows, int* cols, void* stream);
 
 #ifdef __cplusplus
 }

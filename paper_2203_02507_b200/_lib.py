@@ -102,7 +102,7 @@ EXPORTS = [
     "fpmgpu_spectrum_offset_px", "fpmgpu_min_safe_lag", "fpmgpu_build_schedule", "fpmgpu_create",
     "fpmgpu_destroy", "fpmgpu_reconstruct_tiles", "fpmgpu_plan_create", "fpmgpu_plan_execute",
     "fpmgpu_plan_destroy", "fpmgpu_plan_get_info", "fpmgpu_plan_phase_times", "fpmgpu_update_step", "fpmgpu_init_canvas",
-    "fpmgpu_canvas_to_field", "fpmgpu_stitch_mosaic",
+    "fpmgpu_canvas_to_field", "fpmgpu_stitch_mosaic", "fpmgpu_stitch_mosaic_device",
 ]
 
 _lib: C.CDLL | None = None
@@ -134,6 +134,9 @@ def lib() -> C.CDLL:
         L.fpmgpu_canvas_to_field.argtypes = [C.c_void_p, C.POINTER(OpticalConfigC), C.c_void_p, C.c_void_p]
         L.fpmgpu_stitch_mosaic.argtypes = [C.c_void_p, C.POINTER(OpticalConfigC), C.c_void_p, C.c_void_p,
                                            C.c_int, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.fpmgpu_stitch_mosaic_device.argtypes = [C.c_void_p, C.POINTER(OpticalConfigC), C.c_void_p, C.c_void_p,
+                                                  C.c_int, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                                  C.c_void_p]
         _lib = L
     return _lib
 

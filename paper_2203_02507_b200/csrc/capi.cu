@@ -3,6 +3,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <complex>
+#include <map>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -13,6 +15,7 @@
 #include "fpm_b200.h"
 #include "geometry.hpp"
 #include "kernels.cuh"
+#include "stitch.cuh"
 
 using namespace fpmb;
 
@@ -397,6 +400,173 @@ bool same_request(const fpmgpu_context& c, const fpmgpu_recon_request& r, std::v
 
 }  // namespace
 
+namespace {
+
+// Geometry of stitch_mosaic (stitch.cpp:48-86) for a regular tile grid: tiles
+// bucketed into rows by y0 (sorted by x0), cut at the overlap midlines.
+struct StitchLayout {
+    int rows = 0, cols = 0, n_cols = 0, n_strips = 0;
+    std::vector<fpmk::StitchTile> st;
+    std::vector<int> grid;            // [strip][slot] -> tile
+    std::vector<int> X, Y;            // per slot / per strip HR origin
+    std::vector<int> ovh, ovv;        // overlap (HR px) with the previous slot / strip
+    std::vector<int> col_cut, row_cut;
+    std::vector<int> row_of, col_of;  // mosaic row -> strip, column -> slot
+};
+
+StitchLayout stitch_layout(const Cfg& c, const int* xy, int T) {
+    if (T < 1) throw DataError("stitch_mosaic: tile/spec count mismatch");
+    const int up = c.upsample, n = c.tile_size, N = n * up;
+    std::map<int, std::vector<int>> by_row;
+    for (int t = 0; t < T; ++t) by_row[xy[2 * t + 1]].push_back(t);
+    StitchLayout L;
+    std::vector<int> xs;
+    for (auto& kv : by_row) {
+        std::sort(kv.second.begin(), kv.second.end(), [&](int a, int b) { return xy[2 * a] < xy[2 * b]; });
+        std::vector<int> rx;
+        for (int t : kv.second) rx.push_back(xy[2 * t]);
+        if (xs.empty()) xs = rx;
+        else if (rx != xs)
+            throw Unsupported("stitch_mosaic on the device needs every tile row to share its x origins");
+    }
+    std::vector<int> ys;
+    for (auto& kv : by_row) ys.push_back(kv.first);
+    L.n_cols = int(xs.size());
+    L.n_strips = int(ys.size());
+    L.X.resize(size_t(L.n_cols));
+    L.Y.resize(size_t(L.n_strips));
+    L.ovh.assign(size_t(L.n_cols), 0);
+    L.ovv.assign(size_t(L.n_strips), 0);
+    L.col_cut.assign(size_t(L.n_cols) + 1, 0);
+    L.row_cut.assign(size_t(L.n_strips) + 1, 0);
+    for (int k = 0; k < L.n_cols; ++k) {
+        L.X[size_t(k)] = (xs[size_t(k)] - xs[0]) * up;
+        if (k == 0) continue;
+        const int ov = xs[size_t(k) - 1] + n - xs[size_t(k)];
+        if (ov < 0) throw DataError("stitch_mosaic: gap between adjacent tiles");
+        const int width = L.X[size_t(k) - 1] + N;  // strip width before tile k
+        const int o = ov * up;
+        if (o >= width || o >= N) throw DataError("stitch_pair: overlap out of range");
+        L.ovh[size_t(k)] = o;
+        L.col_cut[size_t(k)] = width - o / 2;
+    }
+    L.cols = L.X.back() + N;
+    L.col_cut[size_t(L.n_cols)] = L.cols;
+    for (int k = 0; k < L.n_strips; ++k) {
+        L.Y[size_t(k)] = (ys[size_t(k)] - ys[0]) * up;
+        if (k == 0) continue;
+        const int ov = ys[size_t(k) - 1] + n - ys[size_t(k)];
+        if (ov < 0) throw DataError("stitch_mosaic: gap between tile rows");
+        const int height = L.Y[size_t(k) - 1] + N;
+        const int o = ov * up;
+        if (o >= height || o >= N) throw DataError("stitch_pair: overlap out of range");
+        L.ovv[size_t(k)] = o;
+        L.row_cut[size_t(k)] = height - o / 2;
+    }
+    L.rows = L.Y.back() + N;
+    L.row_cut[size_t(L.n_strips)] = L.rows;
+    L.grid.resize(size_t(L.n_strips) * L.n_cols);
+    L.st.resize(size_t(T));
+    int sidx = 0;
+    for (auto& kv : by_row) {
+        for (int k = 0; k < L.n_cols; ++k) {
+            const int t = kv.second[size_t(k)];
+            L.grid[size_t(sidx) * L.n_cols + k] = t;
+            fpmk::StitchTile& s = L.st[size_t(t)];
+            s.X = L.X[size_t(k)];
+            s.Y = L.Y[size_t(sidx)];
+            s.own_c0 = L.col_cut[size_t(k)] - s.X;
+            s.own_c1 = L.col_cut[size_t(k) + 1] - s.X;
+            s.fre = 1.f;
+            s.fim = 0.f;
+        }
+        ++sidx;
+    }
+    L.row_of.resize(size_t(L.rows));
+    L.col_of.resize(size_t(L.cols));
+    for (int k = 0; k < L.n_strips; ++k)
+        for (int r = L.row_cut[size_t(k)]; r < L.row_cut[size_t(k) + 1]; ++r) L.row_of[size_t(r)] = k;
+    for (int k = 0; k < L.n_cols; ++k)
+        for (int q = L.col_cut[size_t(k)]; q < L.col_cut[size_t(k) + 1]; ++q) L.col_of[size_t(q)] = k;
+    return L;
+}
+
+using C128 = std::complex<double>;
+
+// Ratios of the reference's mean_ratio chain from the per-tile sums, then the
+// assembly pass. colsum/rowsum come back to the host (2 x T x N complex128).
+void stitch_device(fpmgpu_context* ctx, StitchLayout lay, int N, const float2* tiles, float2* out, cudaStream_t s) {
+    const int T = int(lay.st.size());
+    DevBuf<fpmk::StitchTile> st_d;
+    DevBuf<double> colsum_d, rowsum_d;
+    st_d.upload(lay.st.data(), lay.st.size(), s);
+    colsum_d.ensure(size_t(T) * N * 2);
+    rowsum_d.ensure(size_t(T) * N * 2);
+    ck(fpmk::launch_stitch_sums(tiles, st_d.p, T, N, colsum_d.p, rowsum_d.p, s), "stitch sums");
+    std::vector<C128> colsum(size_t(T) * N), rowsum(size_t(T) * N);
+    ck(cudaMemcpyAsync(colsum.data(), colsum_d.p, sizeof(C128) * colsum.size(), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaMemcpyAsync(rowsum.data(), rowsum_d.p, sizeof(C128) * rowsum.size(), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "stitch sums");
+    std::vector<C128> R(size_t(T), C128(1.0, 0.0)), S(size_t(lay.n_strips), C128(1.0, 0.0));
+    // horizontal: ratio of the strip's trailing overlap mean to the tile's leading mean
+    for (int sidx = 0; sidx < lay.n_strips; ++sidx)
+        for (int k = 1; k < lay.n_cols; ++k) {
+            const int o = lay.ovh[size_t(k)];
+            if (o == 0) continue;  // zero overlap concatenates unscaled (stitch.cpp:38)
+            const int t = lay.grid[size_t(sidx) * lay.n_cols + k];
+            C128 m1 = 0.0, m2 = 0.0;
+            for (int C = lay.X[size_t(k)]; C < lay.X[size_t(k)] + o; ++C) {
+                // owner at the time tile k is joined: slot k-1 still reaches the strip's end
+                const int j = lay.grid[size_t(sidx) * lay.n_cols + std::min(lay.col_of[size_t(C)], k - 1)];
+                m1 += R[size_t(j)] * colsum[size_t(j) * N + (C - lay.st[size_t(j)].X)];
+            }
+            for (int q = 0; q < o; ++q) m2 += colsum[size_t(t) * N + q];
+            const double cnt = double(N) * o;
+            if (std::abs(m2 / cnt) < 1e-12) throw DataError("degenerate overlap: |mu2| vanishes");
+            R[size_t(t)] = m1 / m2;
+        }
+    // vertical: the same chain over strips (rows of the assembled strips)
+    auto strip_row = [&](int sidx, int r) {
+        C128 acc = 0.0;
+        for (int k = 0; k < lay.n_cols; ++k) {
+            const int j = lay.grid[size_t(sidx) * lay.n_cols + k];
+            acc += R[size_t(j)] * rowsum[size_t(j) * N + r];
+        }
+        return acc;
+    };
+    for (int k = 1; k < lay.n_strips; ++k) {
+        const int o = lay.ovv[size_t(k)];
+        if (o == 0) continue;
+        C128 m1 = 0.0, m2 = 0.0;
+        for (int Rr = lay.Y[size_t(k)]; Rr < lay.Y[size_t(k)] + o; ++Rr) {
+            const int so = std::min(lay.row_of[size_t(Rr)], k - 1);
+            m1 += S[size_t(so)] * strip_row(so, Rr - lay.Y[size_t(so)]);
+        }
+        for (int r = 0; r < o; ++r) m2 += strip_row(k, r);
+        const double cnt = double(lay.cols) * o;
+        if (std::abs(m2 / cnt) < 1e-12) throw DataError("degenerate overlap: |mu2| vanishes");
+        S[size_t(k)] = m1 / m2;
+    }
+    for (int sidx = 0; sidx < lay.n_strips; ++sidx)
+        for (int k = 0; k < lay.n_cols; ++k) {
+            const int t = lay.grid[size_t(sidx) * lay.n_cols + k];
+            const C128 f = S[size_t(sidx)] * R[size_t(t)];
+            lay.st[size_t(t)].fre = float(f.real());
+            lay.st[size_t(t)].fim = float(f.imag());
+        }
+    DevBuf<int> row_d, col_d, grid_d;
+    st_d.upload(lay.st.data(), lay.st.size(), s);
+    row_d.upload(lay.row_of.data(), lay.row_of.size(), s);
+    col_d.upload(lay.col_of.data(), lay.col_of.size(), s);
+    grid_d.upload(lay.grid.data(), lay.grid.size(), s);
+    ck(fpmk::launch_stitch_assemble(tiles, st_d.p, row_d.p, col_d.p, grid_d.p, lay.n_cols, N, lay.rows, lay.cols,
+                                    out, s), "stitch assemble");
+    ck(cudaStreamSynchronize(s), "stitch assemble");  // the temporaries above are freed on return
+    (void)ctx;
+}
+
+}  // namespace
+
 extern "C" {
 
 int fpmgpu_version(void) { return 1; }
@@ -762,16 +932,34 @@ int fpmgpu_canvas_to_field(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg
 
 int fpmgpu_stitch_mosaic(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const float* tiles, const int* xy,
                          int num_tiles, float* out, int* rows, int* cols) {
-    (void)ctx;
-    (void)cfg;
-    (void)tiles;
-    (void)xy;
-    (void)num_tiles;
-    (void)out;
-    (void)rows;
-    (void)cols;
-    g_err = "stitch_mosaic device kernel not built yet";
-    return FPMGPU_ERR_UNSUPPORTED;
+    return guarded([&] {
+        const StitchLayout lay = stitch_layout(*cfg, xy, num_tiles);
+        *rows = lay.rows;
+        *cols = lay.cols;
+        if (!out) return;
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int N = cfg->tile_size * cfg->upsample;
+        DevBuf<float2> t_d, o_d;
+        t_d.upload(reinterpret_cast<const float2*>(tiles), size_t(num_tiles) * N * N, ctx->stream);
+        o_d.ensure(size_t(lay.rows) * lay.cols);
+        stitch_device(ctx, lay, N, t_d.p, o_d.p, ctx->stream);
+        ck(cudaMemcpyAsync(out, o_d.p, sizeof(float2) * size_t(lay.rows) * lay.cols, cudaMemcpyDeviceToHost,
+                           ctx->stream), "mosaic D2H");
+        ck(cudaStreamSynchronize(ctx->stream), "stitch_mosaic");
+    });
+}
+
+int fpmgpu_stitch_mosaic_device(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const float* tiles_dev,
+                                const int* xy, int num_tiles, float* out_dev, int* rows, int* cols, void* stream) {
+    return guarded([&] {
+        const StitchLayout lay = stitch_layout(*cfg, xy, num_tiles);
+        *rows = lay.rows;
+        *cols = lay.cols;
+        if (!out_dev) return;
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        stitch_device(ctx, lay, cfg->tile_size * cfg->upsample, reinterpret_cast<const float2*>(tiles_dev),
+                      reinterpret_cast<float2*>(out_dev), static_cast<cudaStream_t>(stream));
+    });
 }
 
 }  // extern "C"

@@ -103,3 +103,18 @@ def test_missing_frame_is_data_error():
     t = fpm.partition_tiles(64, 64, cfg)
     with pytest.raises(fpm.DataError, match="missing frame"):
         fpm.make_request(fs, cfg, fpm.led_sequence("spiral", cfg), t, 1)
+
+
+def test_stitch_mosaic_size_query():
+    """Mosaic extents from the device stitch's host layout (no device work):
+    4x4 stock tiles span 946 px (test_stitch.cpp:148-161), toy FOV 120 -> 480."""
+    import ctypes
+    L = _lib.lib()
+    for cfg, fov in ((fpm.OpticalConfig(upsample=1), 946), (fpm.OpticalConfig(tile_size=64, tile_overlap=8), 120)):
+        specs = fpm.partition_tiles(fov, fov, cfg)
+        xy = np.ascontiguousarray([[s.x0, s.y0] for s in specs], np.int32)
+        r, c = ctypes.c_int(), ctypes.c_int()
+        cc = cfg.c()
+        _lib.check(L.fpmgpu_stitch_mosaic(None, ctypes.byref(cc), None, xy.ctypes.data, len(xy), None,
+                                          ctypes.byref(r), ctypes.byref(c)))
+        assert (r.value, c.value) == (fov * cfg.upsample, fov * cfg.upsample)

@@ -188,3 +188,38 @@ def test_offset_out_of_canvas_is_data_error(eng):
     with pytest.raises(fpm.DataError, match="spectrum offset out of canvas bounds"):
         fpm.update_step(canvas, np.ones((64, 64)), (0.95 / cfg.wavelength, 0.0), fpm.build_pupil(cfg, 64),
                         engine=eng)
+
+
+def _stitch_case(orc, cfg, fov, seed, phases=False):
+    rng = np.random.default_rng(seed)
+    up = cfg.upsample
+    whole = (rng.uniform(-1, 1, (fov * up, fov * up)) + 2.0) + 1j * rng.uniform(-1, 1, (fov * up, fov * up))
+    specs = fpm.partition_tiles(fov, fov, cfg)
+    tiles = np.stack([whole[s.y0 * up:(s.y0 + cfg.tile_size) * up, s.x0 * up:(s.x0 + cfg.tile_size) * up]
+                      for s in specs])
+    if phases:
+        tiles = tiles * np.exp(1j * rng.uniform(-np.pi, np.pi, len(specs)))[:, None, None]
+    xy = np.array([[s.x0, s.y0] for s in specs], np.int32)
+    return tiles, xy, specs
+
+
+@pytest.mark.parametrize("fov,ov,phases", [(120, 8, False), (120, 8, True), (121, 8, True), (128, 0, False),
+                                           (200, 24, True)])
+def test_stitch_mosaic_matches_oracle(orc, eng, fov, ov, phases):
+    """Eq. (1) mosaic on the device vs stitch_mosaic (stitch.cpp:48-86), incl. a clamped final tile."""
+    cfg = gpu_cfg(tile_overlap=ov)
+    tiles, xy, specs = _stitch_case(orc, cfg, fov, fov + ov, phases)
+    got = fpm.stitch_mosaic(tiles.astype(np.complex64), specs, cfg, engine=eng)
+    ref = orc.stitch_mosaic(tiles, xy, orc_cfg(cfg))
+    assert got.shape == ref.shape == (fov * 4, fov * 4)
+    assert rel_l2(got, ref) < 1e-5
+
+
+def test_run_offline_stitched_matches_oracle(orc, eng):
+    cfg = gpu_cfg(led_scan_rows=5, led_scan_cols=5, tile_overlap=8)
+    fs, ofs, seq, _ = dataset(cfg, fov=120, seed=32)
+    got = fpm.run_offline(fs, cfg, seq, fpm.RunOptions(iters=2), engine=eng)
+    ref = orc.run_offline(ofs, orc_cfg(cfg), seq, 2)
+    assert got.stitched.shape == ref.stitched.shape == (480, 480)
+    amp, ph = amp_phase_rel(got.stitched, ref.stitched)
+    assert amp < 1e-4 and ph < 1e-4, (amp, ph)
