@@ -156,13 +156,6 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ GPU leg
-def shard(T_rows: int, rank: int, world: int):
-    """Contiguous tile-row band of `rank` (no data-path collective)."""
-    lo = (T_rows * rank) // world
-    hi = (T_rows * (rank + 1)) // world
-    return lo, hi
-
-
 def run_b200(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -174,25 +167,21 @@ def run_b200(args, rank, world):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
+    from paper_2203_02507_b200.distributed import gather_tiles, shard_request
+
     cfg = workload_cfg()
     seq, xy_all, of_all, defocus_all = geometry(cfg)
-    tiles_per_row = FOV // 64
-    rows = FOV // 64
-    r_lo, r_hi = shard(rows, rank, world)
-    t_lo, t_hi = r_lo * tiles_per_row, r_hi * tiles_per_row
-    T = t_hi - t_lo
-    y_lo, y_hi = r_lo * 64, r_hi * 64
-    H = y_hi - y_lo
     L = len(seq)
-    xy = xy_all[t_lo:t_hi].copy()
-    xy[:, 1] -= y_lo
+    full = fpm.Request(cfg, ITERS, xy_all, of_all, np.arange(L, dtype=np.int32), 0, L, FOV, FOV, mode=MODE,
+                       tile_defocus_um=defocus_all)
+    shards = [shard_request(full, r, world) for r in range(world)]
+    me = shards[rank]
+    T, H = len(me.tiles), me.y_hi - me.y_lo
     eng = fpm.Engine(local)
-    req = fpm.Request(cfg, ITERS, xy, of_all[t_lo:t_hi], np.arange(L, dtype=np.int32), 0, L, H, FOV, mode=MODE,
-                      tile_defocus_um=defocus_all[t_lo:t_hi])
-    plan = fpm.Plan(req, eng)
+    plan = fpm.Plan(me.request, eng)
     info = plan.info
 
-    # device-resident synthetic stack (this rank's band), frame k = LED seq[k]
+    # device-resident synthetic stack (this rank's band of LR rows), frame k = LED seq[k]
     g = torch.Generator(device=dev)
     g.manual_seed(1 + rank)
     frames = torch.randint(0, 52429, (L, H, FOV), dtype=torch.int32, device=dev, generator=g).to(torch.uint16)
@@ -200,20 +189,13 @@ def run_b200(args, rank, world):
     hr = torch.empty((T, N, N, 2), dtype=torch.float32, device=dev)
     resid = torch.empty((T, ITERS), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
-    gather_buf = None
-    if world > 1 and rank == 0:
-        gather_buf = [torch.empty(((shard(rows, r, world)[1] - shard(rows, r, world)[0]) * tiles_per_row, N, N, 2),
-                                  dtype=torch.float32, device=dev) for r in range(world)]
+    mosaic_tiles = torch.empty((len(xy_all), N, N, 2), dtype=torch.float32, device=dev) if (
+        world > 1 and rank == 0) else None
 
     def step():
         plan.execute(frames.data_ptr(), FOV, hr.data_ptr(), resid.data_ptr(), None, stream.cuda_stream)
-        if world > 1:  # the only inter-GPU step: HR band gather to rank 0 (NCCL)
-            if rank == 0:
-                gather_buf[0].copy_(hr)
-                for r in range(1, world):
-                    dist.recv(gather_buf[r], src=r)
-            else:
-                dist.send(hr, dst=0)
+        if world > 1:  # the only inter-GPU step: HR tiles gathered to rank 0 (NCCL send/recv)
+            gather_tiles(hr, shards, rank, mosaic_tiles.shape if rank == 0 else None, out=mosaic_tiles)
 
     for _ in range(args.warmup):
         step()
