@@ -135,7 +135,7 @@ void lattice_shape(const std::vector<uint8_t>& support, int* nslots, bool* prune
     }
     (void)mx;
     *prune = inside;
-    *nslots = inside ? 16 : 64;  // lattice positions per thread held in the shared pupil
+    *nslots = inside ? 8 : 32;  // pair-lattice positions per thread held in the shared pupil
 }
 
 std::vector<float2> twiddles(int N) {

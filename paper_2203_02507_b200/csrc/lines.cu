@@ -1,0 +1,190 @@
+// K2/K3 line FFTs (init_canvas, canvas_to_field) and build_pupils.
+#include "fft_device.cuh"
+#include "kernels.cuh"
+
+namespace fpmk {
+
+namespace {
+
+// Radix-4 (+ one radix-2) Stockham passes over `lines` rows of NL points held
+// in shared memory; returns the buffer holding the result.
+template <int NL, bool INV>
+__device__ float2* stockham(float2* s0, float2* s1, int lines, const float2* __restrict__ tw) {
+    float2* src = s0;
+    float2* dst = s1;
+    int Ns = 1;
+#pragma unroll 1
+    for (; Ns * 4 <= NL; Ns *= 4) {
+        const int quarter = NL / 4;
+        const int twstep = NL / (4 * Ns);
+        for (int q = threadIdx.x; q < lines * quarter; q += blockDim.x) {
+            const int line = q / quarter, j = q - line * quarter;
+            const int k = j % Ns;
+            const float2* in = src + line * NL + j;
+            float2 a0 = in[0], a1 = in[quarter], a2 = in[2 * quarter], a3 = in[3 * quarter];
+            if (Ns > 1) {
+                const float2 w1 = __ldg(tw + k * twstep), w2 = __ldg(tw + 2 * k * twstep), w3 = __ldg(tw + 3 * k * twstep);
+                a1 = INV ? cmulc(a1, w1) : cmul(a1, w1);
+                a2 = INV ? cmulc(a2, w2) : cmul(a2, w2);
+                a3 = INV ? cmulc(a3, w3) : cmul(a3, w3);
+            }
+            dft4<INV>(a0, a1, a2, a3);
+            float2* out = dst + line * NL + (j / Ns) * Ns * 4 + k;
+            out[0] = a0;
+            out[Ns] = a1;
+            out[2 * Ns] = a2;
+            out[3 * Ns] = a3;
+        }
+        __syncthreads();
+        float2* tmp = src;
+        src = dst;
+        dst = tmp;
+    }
+    if (Ns < NL) {  // one radix-2 pass (NL = 2 * 4^k)
+        const int half = NL / 2;
+        for (int q = threadIdx.x; q < lines * half; q += blockDim.x) {
+            const int line = q / half, j = q - line * half;
+            const float2 w = __ldg(tw + j);
+            const float2 a0 = src[line * NL + j];
+            const float2 a1 = INV ? cmulc(src[line * NL + j + half], w) : cmul(src[line * NL + j + half], w);
+            dst[line * NL + j] = cadd(a0, a1);
+            dst[line * NL + j + half] = csub(a0, a1);
+        }
+        __syncthreads();
+        src = dst;
+    }
+    return src;
+}
+
+// WHICH 0: init rows    bilinear(sqrt(seed crop)) * C -> FFT rows -> dst
+//       1: init cols    FFT cols of src -> * C * scale -> dst
+//       2: final rows   src * C -> IFFT rows -> dst
+//       3: final cols   IFFT cols of src -> * C * scale -> dst
+template <int NL, int LPB, int WHICH>
+__global__ void __launch_bounds__(256) lines_fft(const LinesArgs a) {
+    constexpr bool INV = WHICH >= 2;
+    constexpr bool COLS = (WHICH & 1) == 1;
+    extern __shared__ float2 lbuf[];
+    float2* s0 = lbuf;
+    float2* s1 = lbuf + LPB * NL;
+    const int tile = blockIdx.y;
+    const int l0 = blockIdx.x * LPB;
+    const size_t base = size_t(tile) * NL * NL;
+
+    for (int idx = threadIdx.x; idx < LPB * NL; idx += blockDim.x) {
+        int line, e;
+        if (COLS) {
+            e = idx / LPB;
+            line = idx - e * LPB;
+        } else {
+            line = idx / NL;
+            e = idx - line * NL;
+        }
+        float2 x;
+        if (WHICH == 0) {
+            // upsample_bilinear (field.cpp:89-112) of the seed crop's sqrt, pixel-centre mapped
+            const int i = l0 + line, j = e, n = a.n;
+            const float fy = (i + 0.5f) / a.up - 0.5f, fx = (j + 0.5f) / a.up - 0.5f;
+            int ya = int(floorf(fy)), xa = int(floorf(fx));
+            const float wy = fy - ya, wx = fx - xa;
+            const int yb = min(ya + 1, n - 1), xb = min(xa + 1, n - 1);
+            ya = max(ya, 0);
+            xa = max(xa, 0);
+            const int2 txy = a.tile_xy[tile];
+            const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
+            const float v00 = sqrtf(float(f[size_t(ya) * a.pitch + xa]));
+            const float v01 = sqrtf(float(f[size_t(ya) * a.pitch + xb]));
+            const float v10 = sqrtf(float(f[size_t(yb) * a.pitch + xa]));
+            const float v11 = sqrtf(float(f[size_t(yb) * a.pitch + xb]));
+            const float val = (1.f - wy) * ((1.f - wx) * v00 + wx * v01) + wy * ((1.f - wx) * v10 + wx * v11);
+            x = make_float2(((i + j) & 1) ? -val : val, 0.f);
+        } else if (COLS) {
+            x = a.src[base + size_t(e) * NL + l0 + line];
+        } else {
+            const int i = l0 + line;
+            x = a.src[base + size_t(i) * NL + e];
+            if (WHICH == 2 && ((i + e) & 1)) x = cneg(x);
+        }
+        s0[line * NL + e] = x;
+    }
+    __syncthreads();
+    const float2* res = stockham<NL, INV>(s0, s1, LPB, a.tw);
+    for (int idx = threadIdx.x; idx < LPB * NL; idx += blockDim.x) {
+        if (COLS) {
+            const int e = idx / LPB, line = idx - e * LPB;
+            const int i = e, j = l0 + line;
+            float2 x = res[line * NL + e];
+            const float sc = ((i + j) & 1) ? -a.scale : a.scale;
+            a.dst[base + size_t(i) * NL + j] = cscale(x, sc);
+        } else {
+            const int line = idx / NL, e = idx - line * NL;
+            a.dst[base + size_t(l0 + line) * NL + e] = res[line * NL + e];
+        }
+    }
+}
+
+template <int NL, int LPB, int WHICH>
+cudaError_t launch_lines_t(const LinesArgs& a, int T, cudaStream_t s) {
+    const size_t smem = size_t(2) * LPB * NL * sizeof(float2);
+    auto k = lines_fft<NL, LPB, WHICH>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    k<<<dim3(NL / LPB, T), 256, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int NL, int LPB>
+cudaError_t launch_lines_n(int which, const LinesArgs& a, int T, cudaStream_t s) {
+    switch (which) {
+        case 0: return launch_lines_t<NL, LPB, 0>(a, T, s);
+        case 1: return launch_lines_t<NL, LPB, 1>(a, T, s);
+        case 2: return launch_lines_t<NL, LPB, 2>(a, T, s);
+        case 3: return launch_lines_t<NL, LPB, 3>(a, T, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+__global__ void build_pupils_kernel(float2* pupils, const uint8_t* support, const double* defocus, int n,
+                                    int T, double dk, double inv_l2) {
+    const size_t total = size_t(T) * n * n;
+    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total; idx += size_t(gridDim.x) * blockDim.x) {
+        const int t = int(idx / (size_t(n) * n));
+        const int p = int(idx % (size_t(n) * n));
+        const int i = p / n, j = p % n;
+        float2 v = make_float2(0.f, 0.f);
+        if (support[p]) {
+            const double z = defocus ? defocus[t] : 0.0;
+            if (z == 0.0) {
+                v = make_float2(1.f, 0.f);
+            } else {  // angular-spectrum defocus phase (optics.cpp:63-67)
+                const double rho = hypot(double(i - n / 2), double(j - n / 2));
+                const double kz = sqrt(fmax(0.0, inv_l2 - rho * dk * rho * dk));
+                double sn, cs;
+                sincos(2.0 * 3.14159265358979323846 * z * kz, &sn, &cs);
+                v = make_float2(float(cs), float(sn));
+            }
+        }
+        pupils[idx] = v;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_lines(int which, int N, const LinesArgs& a, int T, cudaStream_t s) {
+    switch (N) {
+        case 256: return launch_lines_n<256, 16>(which, a, T, s);
+        case 512: return launch_lines_n<512, 8>(which, a, T, s);
+        case 1024: return launch_lines_n<1024, 4>(which, a, T, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_build_pupils(float2* pupils, const uint8_t* support, const double* defocus, int n, int T,
+                                double dk, double inv_l2, cudaStream_t s) {
+    const size_t total = size_t(T) * n * n;
+    const int blocks = int(std::min<size_t>((total + 255) / 256, 148 * 16));
+    build_pupils_kernel<<<blocks, 256, 0, s>>>(pupils, support, defocus, n, T, dk, inv_l2);
+    return cudaGetLastError();
+}
+
+}  // namespace fpmk
