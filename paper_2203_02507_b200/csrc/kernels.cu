@@ -197,6 +197,82 @@ __device__ __forceinline__ void fft64x64_pair(float2 (&v)[8][4], float2* T_s, co
     pair_step2<INV, PRUNE_OUT>(v, sg, tw);
 }
 
+// One forward transform body serves both directions (IFFT(x) = conj(FFT(conj x)),
+// the conjugations folded into gather and modulus), so the update loop carries a
+// single FFT copy: half the instruction footprint of two specialised bodies.
+// The prunings become warp-uniform branches: skip_cols drops the zero columns of
+// the disk-limited input (IFFT), skip_rows the rows the scatter never reads (FFT).
+__device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, const float2* W_s, int p, int h,
+                                                float sg, const float2 (&tw)[4], int g, bool skip_cols,
+                                                bool skip_rows) {
+    const int tr = p >> 3, tc = p & 7;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if ((j == 0 || j == 3) && skip_cols) continue;
+        dft8<false, false>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
+    }
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
+#pragma unroll
+        for (int m = 1; m < 4; ++m) v[a][m] = cmul(v[a][m], tw[m]);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const float2 r = shfl_pair(v[a][m]);
+            v[a][m] = make_float2(fmaf(sg, v[a][m].x, r.x), fmaf(sg, v[a][m].y, r.y));
+        }
+    }
+#pragma unroll
+    for (int a = 1; a < 8; ++a) {
+        const float2 w = W_s[(tr * a) & 63];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) v[a][m] = cmul(v[a][m], w);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const float2 w = W_s[(tc * (4 * h + m)) & 63];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) v[a][m] = cmul(v[a][m], w);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int gm = ((m & 1) << 1) | (((((m >> 1) & 1) ^ h)) << 3);
+        float2* wrow = T_s + (4 * h + m) * 64 + (p ^ gm);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) wrow[a * 512] = v[a][m];
+    }
+    group_sync(g);
+    const int gp = tswz(p);
+    const float2* rrow = T_s + p * 64;
+    const int ofs = (4 * h) ^ (gp & 2);
+    const int rflip = gp & 8;
+#pragma unroll
+    for (int n0r = 0; n0r < 8; ++n0r) {
+        const float2* r = rrow + ((n0r * 8) ^ rflip) + ofs;
+        const float4 q0 = *reinterpret_cast<const float4*>(r);
+        const float4 q1 = *reinterpret_cast<const float4*>(r + (2 ^ (gp & 2)) - (gp & 2));
+        v[n0r][0] = make_float2(q0.x, q0.y);
+        v[n0r][1] = make_float2(q0.z, q0.w);
+        v[n0r][2] = make_float2(q1.x, q1.y);
+        v[n0r][3] = make_float2(q1.z, q1.w);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        dft8<false, false>(v[0][i], v[1][i], v[2][i], v[3][i], v[4][i], v[5][i], v[6][i], v[7][i]);
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        if ((a < 2 || a > 5) && skip_rows) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 r = shfl_pair(v[a][i]);
+            v[a][i] = make_float2(fmaf(sg, v[a][i].x, r.x), fmaf(sg, v[a][i].y, r.y));
+        }
+#pragma unroll
+        for (int i = 1; i < 4; ++i) v[a][i] = cmul(v[a][i], tw[i]);
+        dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
+    }
+}
+
 template <int G>
 __device__ __forceinline__ int2 slot_entry(const LoopArgs& a, int s, int g) {
     if (G == 1) return make_int2(s / a.L, s % a.L);
@@ -343,7 +419,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                     omax = fmaxf(omax, ((mask >> q) & 1u) ? cabs2(O) : 0.f);
                     pmax = fmaxf(pmax, cabs2(P));
                 }
-                v[Lat::a(q)][Lat::j(q)] = cmul(O, P);
+                const float2 c = cmul(O, P);
+                v[Lat::a(q)][Lat::j(q)] = make_float2(c.x, -c.y);  // conj: the IFFT runs as conj(FFT(conj x))
             }
             if (MODE == kModeEPRY) {
 #pragma unroll
@@ -357,8 +434,14 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                 }
             }
 
-            // ---- centered inverse transform (unscaled; 1/n^2 enters only the residual)
-            fft64x64_pair<true, PRUNE, false>(v, T_s, W_s, p, h, sg, tw, g);
+            // ---- pass 0: centered inverse transform (unscaled; 1/n^2 enters only the residual),
+            //      run as conj(FFT(conj x)); modulus replacement
+            // ---- pass 1: centered forward transform of the corrected field
+            float inv_omax = 0.f, inv_pmax = 0.f;
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+            fft64x64_fwd_rt(v, T_s, W_s, p, h, sg, tw, g, PRUNE && pass == 0, PRUNE && pass == 1);
+            if (pass == 1) break;
 
             // ---- modulus replacement with sqrt(I) and residual sums (recon.cpp:115-124):
             // e' = e sqrt(I)/|e| (sqrt(I) + 0i at |e| = 0, recon.cpp:122); the residual is formed
@@ -392,7 +475,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                         const float r = rsqrtf(m2);
                         const float dm = fmaf(m2 * r, inv_n2, -meas);
                         num = fmaf(dm, dm, num);
-                        v[a][u] = cscale(uu, meas * r);
+                        const float sc = meas * r;
+                        v[a][u] = make_float2(uu.x * sc, -uu.y * sc);  // uu = conj(e n^2): undo the conjugation
                     } else {
                         num = fmaf(meas, meas, num);
                         v[a][u] = make_float2(sgn * meas, 0.f);
@@ -423,16 +507,13 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                 const float dsum = (rg[4] + rg[5]) + (rg[6] + rg[7]);
                 stage_sum[e.x] += dsum > 0.f ? double(nsum) / double(dsum) : 0.0;
             }
-            float inv_omax = 0.f, inv_pmax = 0.f;
             if (MODE == kModeEPRY) {
                 const float om = fmaxf(fmaxf(rg[8], rg[9]), fmaxf(rg[10], rg[11]));
                 const float pm = fmaxf(fmaxf(rg[12], rg[13]), fmaxf(rg[14], rg[15]));
                 inv_omax = (om > 0.f && B_s[e.y]) ? args.beta / om : 0.f;  // bright-field pupil steps only
                 inv_pmax = pm > 0.f ? args.alpha / pm : 0.f;
             }
-
-            // ---- centered forward transform of the corrected field
-            fft64x64_pair<false, false, PRUNE>(v, T_s, W_s, p, h, sg, tw, g);
+            }
 
             // ---- scatter into the canvas disk (recon.cpp:127-130) / EPRY update
             if (MODE == kModeGS) {
