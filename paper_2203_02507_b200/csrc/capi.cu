@@ -6,6 +6,7 @@
 #include <complex>
 #include <map>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -138,6 +139,26 @@ void lattice_shape(const std::vector<uint8_t>& support, int* nslots, bool* prune
     *nslots = inside ? 8 : 32;  // pair-lattice positions per thread held in the shared pupil
 }
 
+// Bounding box [b0, b0 + box) of the support disk (same for rows and columns).
+void box_of(const std::vector<uint8_t>& support, int n, int* b0, int* box) {
+    int lo = n, hi = -1;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            if (support[size_t(i) * n + j]) {
+                lo = std::min(lo, std::min(i, j));
+                hi = std::max(hi, std::max(i, j));
+            }
+    if (hi < 0) throw ConfigError("empty pupil support");
+    *b0 = lo;
+    *box = hi - lo + 1;
+}
+
+// FPM_B200_FORCE_BOX=1 runs n = 64 on the general warp-FFT kernel (cross-checks).
+bool box_forced() {
+    const char* e = std::getenv("FPM_B200_FORCE_BOX");
+    return e && e[0] == '1';
+}
+
 std::vector<float2> twiddles(int N) {
     std::vector<float2> w(static_cast<size_t>(N));
     for (int m = 0; m < N; ++m) {
@@ -179,9 +200,11 @@ struct fpmgpu_plan {
     fpmgpu_recon_request req{};
     int n = 0, N = 0, T = 0, L = 0, F = 0, G = 1, lag = 0, nslots = 1, num_slots = 0;
     bool prune = false;
+    bool use_box = false;  // n != 64: warp-FFT box kernel (kernels_box.cu)
+    int box = 0, b0 = 0;
     int support_px = 0;
     double radius = 0.0;
-    DevBuf<float2> canvas, pupils, pupils_init;
+    DevBuf<float2> canvas, pupils, pupils_init, scratch;
     DevBuf<uint8_t> support;
     DevBuf<short2> origins;
     DevBuf<uint8_t> bright;
@@ -222,8 +245,11 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     if (p.T < 1) throw ConfigError("no tiles to reconstruct");
     if (p.L < 1) throw DataError("min_safe_lag: empty sequence");
     p.radius = pupil_radius_px(c, p.n);  // ConfigError on Nyquist / grid checks
-    if (p.n != 64)
-        throw Unsupported("tile side " + std::to_string(p.n) + " has no device kernel in this build (n = 64)");
+    if (p.n != 64 && p.n != 128 && p.n != 256)
+        throw Unsupported("tile side " + std::to_string(p.n) + " has no device kernel in this build (64/128/256)");
+    p.use_box = p.n != 64 || box_forced();
+    if (p.use_box && r.lag != 0)
+        throw Unsupported("the pipelined schedule runs on the n = 64 kernel only in this build");
     if (p.N != 256 && p.N != 512 && p.N != 1024)
         throw Unsupported("canvas side " + std::to_string(p.N) + " has no line-FFT kernel (256/512/1024)");
     for (int t = 0; t < p.T; ++t) {
@@ -252,9 +278,17 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     p.bright.upload(bright.data(), bright.size(), p.ctx->stream);
     p.support_px = 0;
     for (auto s : sup) p.support_px += s;
-    lattice_shape(sup, &p.nslots, &p.prune);
-    if (!p.prune && p.N != 256)
-        throw Unsupported("pupil disk wider than the pruned lattice needs canvas side 256 in this build");
+    if (p.use_box) {
+        box_of(sup, p.n, &p.b0, &p.box);
+        const bool smem_s = p.n != 256;
+        if (p.n == 256 && p.N != 1024) throw Unsupported("n = 256 runs with canvas side 1024 (upsample 4) in this build");
+        if (p.n == 128 && p.N != 512 && p.N != 1024) throw Unsupported("n = 128 needs canvas side 512 or 1024");
+        if (!smem_s) p.scratch.ensure(size_t(p.T) * p.box * (p.n + 1));
+    } else {
+        lattice_shape(sup, &p.nslots, &p.prune);
+        if (!p.prune && p.N != 256)
+            throw Unsupported("pupil disk wider than the pruned lattice needs canvas side 256 in this build");
+    }
 
     // pipelined schedule (parallel.cpp:52-111): one lag for the whole batch,
     // the largest per-tile minimum, so every tile stays sequential-equivalent
@@ -363,7 +397,18 @@ void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* 
     a.nslots = p.nslots;
     a.alpha = float(r.alpha);
     a.beta = float(r.beta);
-    ck(fpmk::launch_loop64(r.mode, p.prune, fpmk::kMeasTMA, p.G, &map, a, p.T, s), "LED loop");
+    if (p.use_box) {
+        fpmk::BoxArgs bx{};
+        bx.scratch = p.scratch.p;
+        bx.frames = frames;
+        bx.pitch = pitch;
+        bx.frame_stride = pitch * r.height;
+        bx.box = p.box;
+        bx.b0 = p.b0;
+        ck(fpmk::launch_loop_box(p.n, r.mode, a, bx, p.T, s), "LED loop (box)");
+    } else {
+        ck(fpmk::launch_loop64(r.mode, p.prune, fpmk::kMeasTMA, p.G, &map, a, p.T, s), "LED loop");
+    }
     if (ev) ck(cudaEventRecord(ev[2], s), "event");
     // canvas_to_field: centered IFFT N x N * up^2 (the 1/N^2 of ifft2 folded in)
     la.src = p.canvas.p;
@@ -743,8 +788,9 @@ int fpmgpu_plan_get_info(const fpmgpu_plan* p, fpmgpu_plan_info* info) {
         info->groups = p->G;
         info->launches_per_execute = (p->has_pupils ? 0 : 1) + 2 + 1 + 2;
         info->loop_ctas = p->T;
-        info->loop_threads = 64 * p->G;
-        info->loop_smem_bytes = int(fpmk::loop_smem_bytes(p->G, p->nslots, p->L, p->req.iters));
+        info->loop_threads = p->use_box ? 512 : 128 * p->G;
+        info->loop_smem_bytes = int(p->use_box ? fpmk::box_smem_bytes(p->n, p->box, p->L, p->req.iters, p->n != 256)
+                                               : fpmk::loop_smem_bytes(p->G, p->nslots, p->L, p->req.iters));
         info->updates = double(p->T) * p->L * p->req.iters;
         info->fft_flops_per_update = 20.0 * p->n * p->n * std::log2(double(p->n));
         info->hbm_bytes_per_update = 2.0 * p->n * p->n + 16.0 * p->support_px;
@@ -812,18 +858,24 @@ int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, fl
     return guarded([&] {
         ck(cudaSetDevice(ctx->device), "cudaSetDevice");
         const int n = cfg->tile_size, N = cfg->tile_size * cfg->upsample;
-        if (n != 64) throw Unsupported("tile side " + std::to_string(n) + " has no device kernel in this build (n = 64)");
+        if (n != 64 && n != 128 && n != 256)
+            throw Unsupported("tile side " + std::to_string(n) + " has no device kernel in this build (64/128/256)");
+        const bool use_box = n != 64 || box_forced();
         auto [oy, ox] = spectrum_offset_px(*cfg, fx, fy);
         const int r0 = N / 2 + oy - n / 2, c0 = N / 2 + ox - n / 2;
         if (r0 < 0 || c0 < 0 || r0 + n > N || c0 + n > N) throw DataError("spectrum offset out of canvas bounds");
         std::vector<uint8_t> sup(size_t(n) * n);
         for (size_t i = 0; i < sup.size(); ++i) sup[i] = pupil[2 * i] != 0.f || pupil[2 * i + 1] != 0.f;
-        int nslots;
-        bool prune;
-        lattice_shape(sup, &nslots, &prune);
+        int nslots = 1, b0 = 0, box = 0;
+        bool prune = false;
         if (N != 256 && N != 512 && N != 1024) throw Unsupported("canvas side " + std::to_string(N) + " unsupported");
-        if (!prune && N != 256)
-            throw Unsupported("pupil disk wider than the pruned lattice needs canvas side 256 in this build");
+        if (use_box) {
+            box_of(sup, n, &b0, &box);
+        } else {
+            lattice_shape(sup, &nslots, &prune);
+            if (!prune && N != 256)
+                throw Unsupported("pupil disk wider than the pruned lattice needs canvas side 256 in this build");
+        }
         cudaStream_t s = ctx->stream;
         DevBuf<float2> cv, pp;
         DevBuf<float> meas;
@@ -864,9 +916,18 @@ int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, fl
         a.nslots = nslots;
         a.alpha = float(alpha);
         a.beta = float(beta);
-        CUtensorMap dummy;
-        std::memset(&dummy, 0, sizeof(dummy));
-        ck(fpmk::launch_loop64(mode, prune, fpmk::kMeasF32, 1, &dummy, a, 1, s), "update_step");
+        DevBuf<float2> scratch;
+        if (use_box) {
+            fpmk::BoxArgs bx{};
+            if (n == 256) bx.scratch = scratch.ensure(size_t(box) * (n + 1));
+            bx.box = box;
+            bx.b0 = b0;
+            ck(fpmk::launch_loop_box(n, mode, a, bx, 1, s), "update_step (box)");
+        } else {
+            CUtensorMap dummy;
+            std::memset(&dummy, 0, sizeof(dummy));
+            ck(fpmk::launch_loop64(mode, prune, fpmk::kMeasF32, 1, &dummy, a, 1, s), "update_step");
+        }
         ck(cudaMemcpyAsync(canvas, cv.p, sizeof(float2) * size_t(N) * N, cudaMemcpyDeviceToHost, s), "canvas D2H");
         if (mode == FPMGPU_MODE_EPRY)
             ck(cudaMemcpyAsync(pupil, pp.p, sizeof(float2) * size_t(n) * n, cudaMemcpyDeviceToHost, s), "pupil D2H");

@@ -40,6 +40,18 @@ struct LinesArgs {
     float scale;
 };
 
+// General tile sides (n = 64, 128, 256): warp-FFT row/column passes over the
+// pupil's bounding box (kernels_box.cu).
+struct BoxArgs {
+    float2* scratch;            // [T][box][n + 1] intermediate when it does not fit shared memory
+    const uint16_t* frames;     // LR stack base, [F][H][pitch]
+    long long pitch;            // elements
+    long long frame_stride;     // elements per frame
+    int box, b0;                // pupil bounding box: rows/cols [b0, b0 + box)
+};
+size_t box_smem_bytes(int n, int box, int L, int iters, bool scratch_in_smem);
+cudaError_t launch_loop_box(int n, int mode, const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s);
+
 size_t loop_smem_bytes(int G, int nslots, int L, int iters);
 cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorMap* tmap,
                           const LoopArgs& a, int T, cudaStream_t s);

@@ -1,0 +1,346 @@
+// fpm_loop_box: the fused per-LED update for LR tile sides n = 32 M (128, 256),
+// persistent over the LED loop like fpm_loop64, one CTA of 16 warps per tile.
+//
+// Every 1-D n-point FFT is done by one warp: a register DFT_M (M = n / 32) and
+// a 32-point DFT across the lanes (5 radix-2 stages over shuffles). Two warp
+// FFT flavours chain without any reordering:
+//   F1: x[l + 32 m] (lane l, register m)      -> X[k0 + M br5(l)] (register k0)
+//       (register DFT, twiddle W_n^(l k0), lane DFT by decimation in frequency)
+//   F2: x[k0 + M br5(l)]                      -> X[q + 32 r] (lane q, register r)
+//       (lane DFT by decimation in time, twiddle W_n^(k0 q), register DFT)
+// The 2-D centred transforms only visit the pupil's bounding box (rows/cols
+// [b0, b0 + B)), which holds every nonzero IFFT input and every FFT output the
+// scatter needs (update_step touches the disk only, recon.cpp:107-130):
+//   A  IFFT of the B box rows (F2, gathered from the canvas disk x P')
+//   B  per column: IFFT (F1) over the B nonzero rows -> modulus with sqrt(I)
+//      -> FFT (F2) -> keep the B box rows
+//   C  FFT of the B box rows (F1) -> scatter into the disk (GS / EPRY)
+// The B x n intermediate lives in shared memory (n = 128: 60 KB) or in a
+// per-tile global scratch (n = 256: 240 KB, L2-resident). Row stride n + 1
+// keeps every column access conflict-free; the staged measurement is
+// XOR-swizzled so the modulus reads (rows k0 + M t) hit 32 distinct banks.
+#include "fft_device.cuh"
+#include "kernels.cuh"
+
+namespace fpmk {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kBoxThreads = 512;
+constexpr int kBoxWarps = kBoxThreads / 32;
+
+__device__ __forceinline__ int brev5(int l) { return int(__brev(unsigned(l)) >> 27); }
+
+__device__ __forceinline__ float2 shfl_x(float2 v, int m) {
+    return make_float2(__shfl_xor_sync(kFull, v.x, m), __shfl_xor_sync(kFull, v.y, m));
+}
+
+template <bool INV>
+__device__ __forceinline__ float2 tmul(float2 v, float2 w) {
+    return INV ? cmulc(v, w) : cmul(v, w);
+}
+
+template <bool INV, int M>
+__device__ __forceinline__ void dftM(float2 (&x)[M]) {
+    if constexpr (M == 2) {
+        const float2 a = x[0], b = x[1];
+        x[0] = cadd(a, b);
+        x[1] = csub(a, b);
+    } else if constexpr (M == 4) {
+        dft4<INV>(x[0], x[1], x[2], x[3]);
+    } else {
+        dft8<INV, false>(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+    }
+}
+
+// Per-lane constants of the warp FFTs: cw[k] = W_(2h)^(l mod h) on the upper
+// lane of the stage h = 2^k (1 on the lower lane), sgk[k] = -1 on the upper
+// lane; tw[k0] = W_n^(l k0).
+template <int M>
+struct WarpFFT {
+    float2 cw[5];
+    float sgk[5];
+    float2 tw[M];
+    __device__ void init(int l, int n) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const int h = 1 << k;
+            const bool up = (l & h) != 0;
+            double s, c;
+            sincospi(-double(l & (h - 1)) / double(h), &s, &c);
+            cw[k] = up ? make_float2(float(c), float(s)) : make_float2(1.f, 0.f);
+            sgk[k] = up ? -1.f : 1.f;
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < M; ++k0) {
+            double s, c;
+            sincospi(-2.0 * double(l * k0) / double(n), &s, &c);
+            tw[k0] = make_float2(float(c), float(s));
+        }
+    }
+    template <bool INV>
+    __device__ __forceinline__ void f1(float2 (&x)[M]) const {
+        dftM<INV, M>(x);
+#pragma unroll
+        for (int k0 = 1; k0 < M; ++k0) x[k0] = tmul<INV>(x[k0], tw[k0]);
+#pragma unroll
+        for (int k = 4; k >= 0; --k) {  // DIF: h = 16 .. 1
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const float2 r = shfl_x(x[k0], 1 << k);
+                const float2 y = make_float2(fmaf(sgk[k], x[k0].x, r.x), fmaf(sgk[k], x[k0].y, r.y));
+                x[k0] = tmul<INV>(y, cw[k]);
+            }
+        }
+    }
+    template <bool INV>
+    __device__ __forceinline__ void f2(float2 (&x)[M]) const {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {  // DIT: h = 1 .. 16
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const float2 b = tmul<INV>(x[k0], cw[k]);
+                const float2 r = shfl_x(b, 1 << k);
+                x[k0] = make_float2(fmaf(sgk[k], b.x, r.x), fmaf(sgk[k], b.y, r.y));
+            }
+        }
+#pragma unroll
+        for (int k0 = 1; k0 < M; ++k0) x[k0] = tmul<INV>(x[k0], tw[k0]);
+        dftM<INV, M>(x);
+    }
+};
+
+}  // namespace
+
+size_t box_smem_bytes(int n, int box, int L, int iters, bool scratch_in_smem) {
+    size_t b = size_t(n) * n * sizeof(uint16_t);                     // swizzled measurement
+    if (scratch_in_smem) b += size_t(box) * (n + 1) * sizeof(float2);  // box-row intermediate
+    b += size_t(iters) * sizeof(double) + 16;
+    b += size_t(kBoxWarps) * 4 * sizeof(float);
+    b += size_t(L) * (sizeof(short2) + sizeof(int) + 1) + 16;
+    return b;
+}
+
+template <int NLR, int MODE, int NC, bool SMEM_S>
+__global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs args, BoxArgs bx) {
+    constexpr int M = NLR / 32;
+    constexpr int RS = NLR + 1;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const int tile = blockIdx.x;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int L = args.L, B = bx.box, b0 = bx.b0;
+    uint8_t* sp = smem_raw;
+    uint16_t* I_s = reinterpret_cast<uint16_t*>(sp);
+    sp += size_t(NLR) * NLR * sizeof(uint16_t);
+    float2* S = nullptr;
+    if constexpr (SMEM_S) {
+        S = reinterpret_cast<float2*>(sp);
+        sp += size_t(B) * RS * sizeof(float2);
+    } else {
+        S = bx.scratch + size_t(tile) * B * RS;
+    }
+    double* stage_sum = reinterpret_cast<double*>(sp);
+    sp += size_t(args.iters) * sizeof(double) + 16;
+    float* red = reinterpret_cast<float*>(sp);  // [warp][4]: num, den, omax, pmax
+    sp += size_t(kBoxWarps) * 4 * sizeof(float);
+    short2* O_s = reinterpret_cast<short2*>(sp);
+    sp += size_t(L) * sizeof(short2);
+    int* F_s = reinterpret_cast<int*>(sp);
+    sp += size_t(L) * sizeof(int);
+    uint8_t* B_s = sp;
+
+    float2* canvas = args.canvas + size_t(tile) * NC * NC;
+    float2* pupil = args.pupils + size_t(tile) * NLR * NLR;
+    const uint8_t* sup = args.support;
+    const int2 txy = args.tile_xy[tile];
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+        O_s[k] = args.origins[size_t(tile) * L + k];
+        F_s[k] = args.seq_frame[k];
+        B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
+    }
+    for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
+    WarpFFT<M> F;
+    F.init(l, NLR);
+    const float inv_n2 = 1.0f / float(NLR * NLR);
+    __syncthreads();
+
+    for (int s = 0; s < args.num_slots; ++s) {
+        const int it = s / L, pos = s % L;
+        const short2 o = O_s[pos];
+        const float2* cvc = canvas + size_t(o.x) * NC + o.y;
+        float2* cv = canvas + size_t(o.x) * NC + o.y;
+
+        // ---- stage the measurement crop, column index XOR 2 (row / M): the modulus
+        // reads rows k0 + M t across the lanes, which then fall in 32 distinct banks
+        if (args.meas_f32 == nullptr) {
+            const uint16_t* fr = bx.frames + size_t(F_s[pos]) * bx.frame_stride + size_t(txy.y) * bx.pitch + txy.x;
+            for (int idx = threadIdx.x; idx < NLR * NLR; idx += kBoxThreads) {
+                const int r = idx / NLR, c = idx % NLR;
+                I_s[r * NLR + (c ^ (2 * (r / M)))] = fr[size_t(r) * bx.pitch + c];
+            }
+        }
+
+        // ---- A: IFFT of the box rows of the disk block (gather x P x checkerboard)
+        float omax = 0.f, pmax = 0.f;
+        for (int i = b0 + w; i < b0 + B; i += kBoxWarps) {
+            float2 x[M];
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const int c = k0 + M * brev5(l);
+                float2 v = make_float2(0.f, 0.f);
+                if (sup[i * NLR + c]) {
+                    const float2 O = cvc[size_t(i) * NC + c];
+                    const float2 P = pupil[i * NLR + c];
+                    v = cscale(cmul(O, P), ((i + c) & 1) ? -1.f : 1.f);
+                    if (MODE == kModeEPRY) {
+                        omax = fmaxf(omax, cabs2(O));
+                        pmax = fmaxf(pmax, cabs2(P));
+                    }
+                }
+                x[k0] = v;
+            }
+            F.template f2<true>(x);
+#pragma unroll
+            for (int r = 0; r < M; ++r) S[size_t(i - b0) * RS + l + 32 * r] = x[r];
+        }
+        if (MODE == kModeEPRY) {
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                omax = fmaxf(omax, __shfl_xor_sync(kFull, omax, sh));
+                pmax = fmaxf(pmax, __shfl_xor_sync(kFull, pmax, sh));
+            }
+            if (l == 0) {
+                red[w * 4 + 2] = omax;
+                red[w * 4 + 3] = pmax;
+            }
+        }
+        __syncthreads();
+
+        // ---- B: per column, IFFT over the box rows -> modulus -> FFT -> keep the box rows
+        float num = 0.f, den = 0.f;
+        for (int j = w; j < NLR; j += kBoxWarps) {
+            float2 x[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const int r = l + 32 * m;
+                x[m] = (r >= b0 && r < b0 + B) ? S[size_t(r - b0) * RS + j] : make_float2(0.f, 0.f);
+            }
+            F.template f1<true>(x);
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const int row = k0 + M * brev5(l);
+                float Iv;
+                if (args.meas_f32 == nullptr) {
+                    Iv = float(I_s[row * NLR + (j ^ (2 * (row / M)))]);
+                } else {
+                    Iv = args.meas_f32[row * NLR + j];
+                }
+                den += Iv;
+                float meas;
+                asm("sqrt.approx.f32 %0, %1;" : "=f"(meas) : "f"(Iv));
+                const float2 u = x[k0];
+                const float m2 = cabs2(u);
+                if (m2 > 0.f) {
+                    const float rr = rsqrtf(m2);
+                    const float dm = fmaf(m2 * rr, inv_n2, -meas);
+                    num = fmaf(dm, dm, num);
+                    x[k0] = cscale(u, meas * rr);
+                } else {
+                    num = fmaf(meas, meas, num);
+                    x[k0] = make_float2(((row + j) & 1) ? -meas : meas, 0.f);
+                }
+            }
+            F.template f2<false>(x);
+#pragma unroll
+            for (int r = 0; r < M; ++r) {
+                const int row = l + 32 * r;
+                if (row >= b0 && row < b0 + B) S[size_t(row - b0) * RS + j] = x[r];
+            }
+        }
+#pragma unroll
+        for (int sh = 16; sh; sh >>= 1) {
+            num += __shfl_xor_sync(kFull, num, sh);
+            den += __shfl_xor_sync(kFull, den, sh);
+        }
+        if (l == 0) {
+            red[w * 4] = num;
+            red[w * 4 + 1] = den;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float nsum = 0.f, dsum = 0.f;
+            for (int k = 0; k < kBoxWarps; ++k) {
+                nsum += red[k * 4];
+                dsum += red[k * 4 + 1];
+            }
+            stage_sum[it] += dsum > 0.f ? double(nsum) / double(dsum) : 0.0;
+        }
+        float inv_omax = 0.f, inv_pmax = 0.f;
+        if (MODE == kModeEPRY) {
+            float om = 0.f, pm = 0.f;
+            for (int k = 0; k < kBoxWarps; ++k) {
+                om = fmaxf(om, red[k * 4 + 2]);
+                pm = fmaxf(pm, red[k * 4 + 3]);
+            }
+            inv_omax = (om > 0.f && B_s[pos]) ? args.beta / om : 0.f;  // bright-field pupil steps only
+            inv_pmax = pm > 0.f ? args.alpha / pm : 0.f;
+        }
+
+        // ---- C: FFT of the box rows, scatter into the disk (recon.cpp:127-130) / EPRY
+        for (int i = b0 + w; i < b0 + B; i += kBoxWarps) {
+            float2 x[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) x[m] = S[size_t(i - b0) * RS + l + 32 * m];
+            F.template f1<false>(x);
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const int c = k0 + M * brev5(l);
+                if (!sup[i * NLR + c]) continue;
+                const float2 psi2 = cscale(x[k0], ((i + c) & 1) ? -1.f : 1.f);
+                float2* dst = cv + size_t(i) * NC + c;
+                float2* pp = pupil + i * NLR + c;
+                const float2 P = *pp;
+                if (MODE == kModeGS) {
+                    *dst = cmulc(psi2, P);
+                } else {
+                    const float2 O = *dst;
+                    const float2 d = csub(psi2, cmul(O, P));
+                    if (inv_pmax > 0.f) *dst = cadd(O, cscale(cmulc(d, P), inv_pmax));
+                    if (inv_omax > 0.f) *pp = cadd(P, cscale(cmulc(d, O), inv_omax));
+                }
+            }
+        }
+        __syncthreads();  // canvas, pupil and reductions settled before the next update
+    }
+    for (int k = threadIdx.x; k < args.iters; k += blockDim.x)
+        args.residuals[size_t(tile) * args.iters + k] = stage_sum[k] / double(L);
+}
+
+template <int NLR, int MODE, int NC, bool SMEM_S>
+static cudaError_t launch_box_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s) {
+    const size_t smem = box_smem_bytes(NLR, b.box, a.L, a.iters, SMEM_S);
+    auto k = fpm_loop_box<NLR, MODE, NC, SMEM_S>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    k<<<T, kBoxThreads, smem, s>>>(a, b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loop_box(int n, int mode, const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s) {
+#define FPM_BOX_CASE(NN, MM, NCC, SM)                       \
+    if (n == NN && mode == MM && a.N == NCC)               \
+        return launch_box_t<NN, MM, NCC, SM>(a, b, T, s);
+    FPM_BOX_CASE(128, kModeGS, 512, true)
+    FPM_BOX_CASE(128, kModeEPRY, 512, true)
+    FPM_BOX_CASE(128, kModeGS, 1024, true)
+    FPM_BOX_CASE(128, kModeEPRY, 1024, true)
+    FPM_BOX_CASE(256, kModeGS, 1024, false)
+    FPM_BOX_CASE(256, kModeEPRY, 1024, false)
+    FPM_BOX_CASE(64, kModeGS, 256, true)
+    FPM_BOX_CASE(64, kModeEPRY, 256, true)
+#undef FPM_BOX_CASE
+    return cudaErrorInvalidConfiguration;
+}
+
+}  // namespace fpmk

@@ -223,3 +223,68 @@ def test_run_offline_stitched_matches_oracle(orc, eng):
     assert got.stitched.shape == ref.stitched.shape == (480, 480)
     amp, ph = amp_phase_rel(got.stitched, ref.stitched)
     assert amp < 1e-4 and ph < 1e-4, (amp, ph)
+
+
+# ---------------------------------------------------------------- n = 128 / 256 (box kernel)
+def _single_tile(n, scan, seed, defocus=0.0):
+    cfg = fpm.OpticalConfig(tile_size=n, tile_overlap=0, upsample=4, led_scan_rows=scan, led_scan_cols=scan)
+    fs, ofs, seq, _ = dataset(cfg, seed=seed, defocus_um=defocus)
+    return cfg, fs, ofs, seq, fpm.partition_tiles(n, n, cfg)[0]
+
+
+@pytest.mark.parametrize("mode,iters", [("gs", 1), ("epry", 1), ("epry", 2)])
+def test_n128_per_iteration(orc, eng, mode, iters):
+    """Config 2 geometry (128x128 LR, 15x15 LEDs) per iteration, GS and EPRY."""
+    cfg, fs, ofs, seq, t = _single_tile(128, 15, seed=2, defocus=15.0)
+    got = fpm.reconstruct_tile(fs, t, cfg, iters, seq, mode=mode, engine=eng)
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), iters, seq, mode=mode)
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
+    assert np.allclose(got.metrics.pass_mean_residual, ref.residuals, rtol=1e-3)
+
+
+def test_config2_full_epry(orc, eng):
+    """BASELINE config 2: single 128x128 tile, 15x15 LEDs, EPRY, 20 iterations."""
+    cfg, fs, ofs, seq, t = _single_tile(128, 15, seed=1, defocus=15.0)
+    got = fpm.reconstruct_tile(fs, t, cfg, 20, seq, mode="epry", engine=eng)
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), 20, seq, mode="epry")
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < FINAL_TOL and ph < FINAL_TOL, (amp, ph)
+    assert rel_l2(got.pupil, ref.pupil) < FINAL_TOL
+
+
+@pytest.mark.parametrize("mode", ["gs", "epry"])
+def test_n256_config5_geometry(orc, eng, mode):
+    """Config 5 tile geometry: 256x256 LR (N = 1024), 21x21 LEDs."""
+    cfg, fs, ofs, seq, t = _single_tile(256, 21, seed=5, defocus=10.0)
+    got = fpm.reconstruct_tile(fs, t, cfg, 2, seq, mode=mode, engine=eng)
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), 2, seq, mode=mode)
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
+    assert np.allclose(got.metrics.pass_mean_residual, ref.residuals, rtol=1e-3)
+
+
+@pytest.mark.parametrize("n", [128, 256])
+def test_update_step_box_matches_oracle(orc, eng, n):
+    cfg, fs, ofs, seq, t = _single_tile(n, 5, seed=7)
+    canvas = orc.init_canvas(ofs, orc_cfg(cfg))
+    pupil = fpm.build_pupil(cfg, n, 6.0)
+    for led in seq[:4]:
+        I = fs.images[fs.find(led)].astype(np.float64)
+        gc = fpm.SpectrumCanvas(canvas.astype(np.complex64), cfg)
+        r_gpu = fpm.update_step(gc, I, t.wavevectors[led], pupil, engine=eng)
+        r_ref = orc.update_step(canvas, I, t.wavevectors[led], pupil.values, orc_cfg(cfg))
+        assert r_gpu == pytest.approx(r_ref, rel=1e-4, abs=1e-9)
+        assert rel_l2(gc.spectrum, canvas) < 1e-5
+
+
+def test_box_kernel_agrees_with_lattice_kernel_n64(eng, monkeypatch):
+    """The general warp-FFT kernel and the n = 64 lattice kernel compute the same update."""
+    cfg = gpu_cfg(led_scan_rows=9, led_scan_cols=9, tile_overlap=8)
+    fs, _, seq, _ = dataset(cfg, fov=120, seed=33)
+    opt = fpm.RunOptions(iters=2, mode="epry", tile_defocus_um=[3.0, -2.0, 0.0, 5.0])
+    a = fpm.run_offline(fs, cfg, seq, opt, engine=eng, stitch=False)
+    monkeypatch.setenv("FPM_B200_FORCE_BOX", "1")
+    b = fpm.run_offline(fs, cfg, seq, opt, engine=fpm.Engine(0), stitch=False)
+    for i in range(4):
+        assert rel_l2(b.tiles[i], a.tiles[i]) < 1e-5
