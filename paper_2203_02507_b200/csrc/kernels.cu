@@ -88,87 +88,41 @@ __device__ __forceinline__ int tswz(int pp) {
     return ((pp & 1) << 1) | ((((pp >> 1) ^ (pp >> 2)) & 1) << 3);
 }
 
-template <bool INV>
-__device__ __forceinline__ float2 twmul(float2 v, float2 w) {
-    return INV ? cmulc(v, w) : cmul(v, w);
-}
-
-// DFT4, natural order; MID2: inputs 0 and 3 are known zero.
-template <bool INV, bool MID2>
-__device__ __forceinline__ void dft4p(float2& a0, float2& a1, float2& a2, float2& a3) {
-    if (MID2) {
-        const float2 d13 = w8_2<INV>(a1);
-        const float2 x1 = a1, x2 = a2;
-        a0 = cadd(x2, x1);
-        a2 = csub(x2, x1);
-        a1 = csub(d13, x2);
-        a3 = make_float2(-x2.x - d13.x, -x2.y - d13.y);
-    } else {
-        dft4<INV>(a0, a1, a2, a3);
-    }
-}
-
-// Step 1 on the pair lattice: v[a][j] = x[n1r = a][n1c = 2j + h].
-// Out: v[k0r][m] with k0c = 4h + m. PRUNE_IN: only a, b in [2, 6) nonzero.
-template <bool INV, bool PRUNE_IN>
-__device__ __forceinline__ void pair_step1(float2 (&v)[8][4], float sg, const float2 (&tw)[4]) {
+// One forward transform body serves both directions (IFFT(x) = conj(FFT(conj x)),
+// the conjugations folded into gather and modulus), so the update loop carries a
+// single FFT copy: half the instruction footprint of two specialised bodies.
+// The prunings become warp-uniform branches: skip_cols drops the zero columns of
+// the disk-limited input (IFFT), skip_rows the rows the scatter never reads (FFT).
+__device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, const float4* W4_s, int p, int h,
+                                                float sg, const float2 (&tw)[4], const float2 (&twsw)[4], int g,
+                                                bool skip_cols, bool skip_rows) {
+    const int tr = p >> 3, tc = p & 7;
+    // step 1: DFT8 over n1r (registers), then the pair DFT over n1c (DIT)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        if (PRUNE_IN && (j == 0 || j == 3)) continue;
-        dft8<INV, PRUNE_IN>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
+        if ((j == 0 || j == 3) && skip_cols) continue;
+        dft8<false, false>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
     }
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
-        dft4p<INV, PRUNE_IN>(v[a][0], v[a][1], v[a][2], v[a][3]);  // E (h = 0) or O (h = 1)
+        dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);  // E (h = 0) or O (h = 1)
 #pragma unroll
-        for (int m = 1; m < 4; ++m) v[a][m] = twmul<INV>(v[a][m], tw[m]);  // O' = W8^m O (tw = 1 on h = 0)
+        for (int m = 1; m < 4; ++m) v[a][m] = cmul_sw(v[a][m], tw[m], twsw[m]);  // O' = W8^m O
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {  // h = 0: E + O'; h = 1: E - O'
-            const float2 r = shfl_pair(v[a][m]);
-            v[a][m] = make_float2(fmaf(sg, v[a][m].x, r.x), fmaf(sg, v[a][m].y, r.y));
-        }
+        for (int m = 0; m < 4; ++m) v[a][m] = cfma(sg, v[a][m], shfl_pair(v[a][m]));  // E + O' | E - O'
     }
-}
-
-// Step 2: v[n0r][i] = y[n0r][n0c = 4h + i]. Out: v[k1r][u] with k1c = 2u + h.
-// PRUNE_OUT: only output rows k1r in [2, 6) are consumed.
-template <bool INV, bool PRUNE_OUT>
-__device__ __forceinline__ void pair_step2(float2 (&v)[8][4], float sg, const float2 (&tw)[4]) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        dft8<INV, false>(v[0][i], v[1][i], v[2][i], v[3][i], v[4][i], v[5][i], v[6][i], v[7][i]);
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        if (PRUNE_OUT && (a < 2 || a > 5)) continue;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {  // h = 0: y_i + y_(i+4); h = 1: y_i - y_(i+4)
-            const float2 r = shfl_pair(v[a][i]);
-            v[a][i] = make_float2(fmaf(sg, v[a][i].x, r.x), fmaf(sg, v[a][i].y, r.y));
-        }
-#pragma unroll
-        for (int i = 1; i < 4; ++i) v[a][i] = twmul<INV>(v[a][i], tw[i]);
-        dft4<INV>(v[a][0], v[a][1], v[a][2], v[a][3]);
-    }
-}
-
-// Full centred-core 64x64 transform on the pair lattice (signs folded by the caller).
-template <bool INV, bool PRUNE_IN, bool PRUNE_OUT>
-__device__ __forceinline__ void fft64x64_pair(float2 (&v)[8][4], float2* T_s, const float2* W_s, int p, int h,
-                                              float sg, const float2 (&tw)[4], int g) {
-    const int tr = p >> 3, tc = p & 7;
-    pair_step1<INV, PRUNE_IN>(v, sg, tw);
-    // twiddle W64^(n0r k0r + n0c k0c), k0 = (a, 4h + m)
+    // twiddle W64^(n0r k0r + n0c k0c), k0 = (a, 4h + m); table entries (w, (-w.y, w.x))
 #pragma unroll
     for (int a = 1; a < 8; ++a) {
-        const float2 w = W_s[(tr * a) & 63];
+        const float4 w = W4_s[(tr * a) & 63];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) v[a][m] = twmul<INV>(v[a][m], w);
+        for (int m = 0; m < 4; ++m) v[a][m] = cmul_sw(v[a][m], make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        const float2 w = W_s[(tc * (4 * h + m)) & 63];
+        const float4 w = W4_s[(tc * (4 * h + m)) & 63];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) v[a][m] = twmul<INV>(v[a][m], w);
+        for (int a = 0; a < 8; ++a) v[a][m] = cmul_sw(v[a][m], make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
     // transpose: element k0 = (a, 4h + m) of residue p goes to row p' = 8a + 4h + m, slot p
 #pragma unroll
@@ -194,68 +148,7 @@ __device__ __forceinline__ void fft64x64_pair(float2 (&v)[8][4], float2* T_s, co
         v[n0r][2] = make_float2(q1.x, q1.y);
         v[n0r][3] = make_float2(q1.z, q1.w);
     }
-    pair_step2<INV, PRUNE_OUT>(v, sg, tw);
-}
-
-// One forward transform body serves both directions (IFFT(x) = conj(FFT(conj x)),
-// the conjugations folded into gather and modulus), so the update loop carries a
-// single FFT copy: half the instruction footprint of two specialised bodies.
-// The prunings become warp-uniform branches: skip_cols drops the zero columns of
-// the disk-limited input (IFFT), skip_rows the rows the scatter never reads (FFT).
-__device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, const float2* W_s, int p, int h,
-                                                float sg, const float2 (&tw)[4], int g, bool skip_cols,
-                                                bool skip_rows) {
-    const int tr = p >> 3, tc = p & 7;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if ((j == 0 || j == 3) && skip_cols) continue;
-        dft8<false, false>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
-    }
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
-#pragma unroll
-        for (int m = 1; m < 4; ++m) v[a][m] = cmul(v[a][m], tw[m]);
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const float2 r = shfl_pair(v[a][m]);
-            v[a][m] = make_float2(fmaf(sg, v[a][m].x, r.x), fmaf(sg, v[a][m].y, r.y));
-        }
-    }
-#pragma unroll
-    for (int a = 1; a < 8; ++a) {
-        const float2 w = W_s[(tr * a) & 63];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) v[a][m] = cmul(v[a][m], w);
-    }
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        const float2 w = W_s[(tc * (4 * h + m)) & 63];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) v[a][m] = cmul(v[a][m], w);
-    }
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        const int gm = ((m & 1) << 1) | (((((m >> 1) & 1) ^ h)) << 3);
-        float2* wrow = T_s + (4 * h + m) * 64 + (p ^ gm);
-#pragma unroll
-        for (int a = 0; a < 8; ++a) wrow[a * 512] = v[a][m];
-    }
-    group_sync(g);
-    const int gp = tswz(p);
-    const float2* rrow = T_s + p * 64;
-    const int ofs = (4 * h) ^ (gp & 2);
-    const int rflip = gp & 8;
-#pragma unroll
-    for (int n0r = 0; n0r < 8; ++n0r) {
-        const float2* r = rrow + ((n0r * 8) ^ rflip) + ofs;
-        const float4 q0 = *reinterpret_cast<const float4*>(r);
-        const float4 q1 = *reinterpret_cast<const float4*>(r + (2 ^ (gp & 2)) - (gp & 2));
-        v[n0r][0] = make_float2(q0.x, q0.y);
-        v[n0r][1] = make_float2(q0.z, q0.w);
-        v[n0r][2] = make_float2(q1.x, q1.y);
-        v[n0r][3] = make_float2(q1.z, q1.w);
-    }
+    // step 2: DFT8 over n0r, then the pair DFT over n0c (DIF)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
         dft8<false, false>(v[0][i], v[1][i], v[2][i], v[3][i], v[4][i], v[5][i], v[6][i], v[7][i]);
@@ -263,12 +156,9 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
     for (int a = 0; a < 8; ++a) {
         if ((a < 2 || a > 5) && skip_rows) continue;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float2 r = shfl_pair(v[a][i]);
-            v[a][i] = make_float2(fmaf(sg, v[a][i].x, r.x), fmaf(sg, v[a][i].y, r.y));
-        }
+        for (int i = 0; i < 4; ++i) v[a][i] = cfma(sg, v[a][i], shfl_pair(v[a][i]));  // y_i + y_(i+4) | y_i - y_(i+4)
 #pragma unroll
-        for (int i = 1; i < 4; ++i) v[a][i] = cmul(v[a][i], tw[i]);
+        for (int i = 1; i < 4; ++i) v[a][i] = cmul_sw(v[a][i], tw[i], twsw[i]);
         dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
     }
 }
@@ -295,7 +185,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
     size_t b = 1024;                                              // alignment slack (128B-swizzled TMA box)
     b += size_t(G) * kGroupBytes;                                 // per-group staging + transpose
     b += size_t(nslots) * kGroupThreads * sizeof(float2);         // lattice pupil [NP][128]
-    b += 64 * sizeof(float2);                                     // W64 table
+    b += 64 * sizeof(float4);                                     // W64 table (+ swizzled copy)
     b += size_t(iters) * sizeof(double);                          // stage sums
     b += size_t(G) * (sizeof(uint64_t) + 16 * sizeof(float));     // mbarriers + reductions
     b += size_t(L) * (sizeof(short2) + sizeof(int) + 1);          // origins + frame map + bright flags
@@ -324,8 +214,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
     size_t off = size_t(G) * kGroupBytes;
     float2* P_s = reinterpret_cast<float2*>(smem + off);  // [NP][128], P' = (-1)^(i+j) P, zero off the support
     off += size_t(NP) * kGroupThreads * sizeof(float2);
-    float2* W_s = reinterpret_cast<float2*>(smem + off);  // W64^m, m in [0, 64)
-    off += 64 * sizeof(float2);
+    float4* W4_s = reinterpret_cast<float4*>(smem + off);  // (W64^m, swizzled W64^m), m in [0, 64)
+    off += 64 * sizeof(float4);
     double* stage_sum = reinterpret_cast<double*>(smem + off);
     off += size_t(args.iters) * sizeof(double);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off);
@@ -363,7 +253,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
     if (threadIdx.x < 64) {
         double s, c;
         sincospi(-double(threadIdx.x) / 32.0, &s, &c);
-        W_s[threadIdx.x] = make_float2(float(c), float(s));
+        W4_s[threadIdx.x] = make_float4(float(c), float(s), -float(s), float(c));
     }
     // pair-combine twiddles W8^m, m = 1..3, on the odd lane (1 on the even lane)
     float2 tw[4];
@@ -374,6 +264,9 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
         tw[2] = h ? make_float2(0.f, -1.f) : make_float2(1.f, 0.f);
         tw[3] = h ? make_float2(-s, -s) : make_float2(1.f, 0.f);
     }
+    float2 twsw[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) twsw[m] = make_float2(-tw[m].y, tw[m].x);
     const float sg = h ? -1.f : 1.f;
     if (MEAS == kMeasTMA && tl == 0) {
         mbar_init(bar, 1);
@@ -440,7 +333,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
             float inv_omax = 0.f, inv_pmax = 0.f;
 #pragma unroll 1
             for (int pass = 0; pass < 2; ++pass) {
-            fft64x64_fwd_rt(v, T_s, W_s, p, h, sg, tw, g, PRUNE && pass == 0, PRUNE && pass == 1);
+            fft64x64_fwd_rt(v, T_s, W4_s, p, h, sg, tw, twsw, g, PRUNE && pass == 0, PRUNE && pass == 1);
             if (pass == 1) break;
 
             // ---- modulus replacement with sqrt(I) and residual sums (recon.cpp:115-124):
