@@ -69,6 +69,20 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
 }
 __device__ __forceinline__ float cabs2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
 
+// Single-MUFU approximations without the denormal pre/post scaling of the
+// non-ftz forms; callers clamp their arguments to >= kTiny (or 0 for sqrt).
+constexpr float kTiny = 1.17549435e-38f;  // FLT_MIN
+__device__ __forceinline__ float sqrt_ftz(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // multiply by W8^2 = -i (fwd) / +i (inv): a swap and a sign, folded into the consumer
 template <bool INV>
 __device__ __forceinline__ float2 w8_2(float2 a) {

@@ -360,20 +360,17 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                         Iv = args.meas_f32[(tr + 8 * a) * 64 + tc + 8 * b];
                         den_f += Iv;
                     }
-                    float meas;  // sqrt(I): one MUFU.SQRT (exact 0 at I = 0)
-                    asm("sqrt.approx.f32 %0, %1;" : "=f"(meas) : "f"(Iv));
+                    // branch-free: |e|^2 at or below FLT_MIN counts as |e| = 0 (recon.cpp:122)
+                    const float meas = sqrt_ftz(Iv);
                     const float2 uu = v[a][u];
                     const float m2 = cabs2(uu);
-                    if (__builtin_expect(m2 > 0.f, 1)) {
-                        const float r = rsqrtf(m2);
-                        const float dm = fmaf(m2 * r, inv_n2, -meas);
-                        num = fmaf(dm, dm, num);
-                        const float sc = meas * r;
-                        v[a][u] = make_float2(uu.x * sc, -uu.y * sc);  // uu = conj(e n^2): undo the conjugation
-                    } else {
-                        num = fmaf(meas, meas, num);
-                        v[a][u] = make_float2(sgn * meas, 0.f);
-                    }
+                    const bool nz = m2 > kTiny;
+                    const float r = rsqrt_ftz(fmaxf(m2, kTiny));
+                    const float dm = fmaf(m2 * r, inv_n2, -meas);  // |e| - sqrt(I)
+                    num = fmaf(dm, dm, num);
+                    const float sc = nz ? meas * r : 0.f;
+                    // uu = conj(e n^2): undo the conjugation; the zero case becomes sqrt(I) + 0i
+                    v[a][u] = make_float2(fmaf(uu.x, sc, nz ? 0.f : sgn * meas), -uu.y * sc);
                 }
             float den = MEAS == kMeasTMA ? float(den_u) : den_f;
 #pragma unroll

@@ -237,19 +237,17 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
                     Iv = args.meas_f32[row * NLR + j];
                 }
                 den += Iv;
-                float meas;
-                asm("sqrt.approx.f32 %0, %1;" : "=f"(meas) : "f"(Iv));
+                // branch-free: |e|^2 at or below FLT_MIN counts as |e| = 0 (recon.cpp:122)
+                const float meas = sqrt_ftz(Iv);
                 const float2 u = x[k0];
                 const float m2 = cabs2(u);
-                if (m2 > 0.f) {
-                    const float rr = rsqrtf(m2);
-                    const float dm = fmaf(m2 * rr, inv_n2, -meas);
-                    num = fmaf(dm, dm, num);
-                    x[k0] = cscale(u, meas * rr);
-                } else {
-                    num = fmaf(meas, meas, num);
-                    x[k0] = make_float2(((row + j) & 1) ? -meas : meas, 0.f);
-                }
+                const bool nz = m2 > kTiny;
+                const float rr = rsqrt_ftz(fmaxf(m2, kTiny));
+                const float dm = fmaf(m2 * rr, inv_n2, -meas);
+                num = fmaf(dm, dm, num);
+                const float sc = nz ? meas * rr : 0.f;
+                const float z = nz ? 0.f : (((row + j) & 1) ? -meas : meas);
+                x[k0] = make_float2(fmaf(u.x, sc, z), u.y * sc);
             }
             F.template f2<false>(x);
 #pragma unroll
