@@ -179,7 +179,11 @@ struct fpmgpu_context {
     DevBuf<float2> hr;
     DevBuf<double> resid;
     DevBuf<float2> pup;
-    fpmgpu_plan* cached = nullptr;
+    // host path: one cached plan per tile band, band b = tiles [band_t0[b], band_t0[b+1])
+    std::vector<fpmgpu_plan*> cached;
+    std::vector<int> band_t0;
+    std::vector<cudaStream_t> band_streams;
+    std::vector<cudaEvent_t> band_events;
     std::vector<int> cached_key_i;
     std::vector<double> cached_key_d;
     std::vector<float> cached_key_f;
@@ -440,7 +444,7 @@ bool same_request(const fpmgpu_context& c, const fpmgpu_recon_request& r, std::v
     kd.push_back(r.beta);
     if (r.tile_defocus_um) kd.insert(kd.end(), r.tile_defocus_um, r.tile_defocus_um + r.num_tiles);
     if (r.pupils) kf.insert(kf.end(), r.pupils, r.pupils + 2 * size_t(r.num_tiles) * r.cfg.tile_size * r.cfg.tile_size);
-    return c.cached && ki == c.cached_key_i && kd == c.cached_key_d && kf == c.cached_key_f;
+    return !c.cached.empty() && ki == c.cached_key_i && kd == c.cached_key_d && kf == c.cached_key_f;
 }
 
 }  // namespace
@@ -745,7 +749,12 @@ int fpmgpu_destroy(fpmgpu_context* ctx) {
     return guarded([&] {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
-        if (ctx->cached) delete ctx->cached;
+        for (auto* p : ctx->cached) delete p;
+        for (auto s : ctx->band_streams) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+        for (auto e : ctx->band_events) cudaEventDestroy(e);
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
@@ -814,6 +823,34 @@ int fpmgpu_plan_phase_times(fpmgpu_plan* plan, double* ms, int* executes, int re
     });
 }
 
+namespace {
+
+// Host-path banding: the tiles are cut into contiguous index chunks at tile-row
+// changes (row-major partitions make each chunk a horizontal band of the FOV),
+// so band b's LR rows can cross PCIe while band b-1 already reconstructs and
+// band b-2's HR tiles travel back. FPM_B200_BANDS overrides the count (1 = off).
+// The pipelined schedule picks ONE lag for the whole batch, so it stays unbanded.
+std::vector<int> host_bands(const fpmgpu_recon_request& r) {
+    const int T = r.num_tiles;
+    int want = 8;
+    if (const char* e = std::getenv("FPM_B200_BANDS")) want = std::max(1, std::atoi(e));
+    std::vector<int> row_start;  // tile indices where a new tile row begins
+    for (int t = 0; t < T; ++t)
+        if (t == 0 || r.tile_xy[2 * t + 1] != r.tile_xy[2 * t - 1]) row_start.push_back(t);
+    const int rows = int(row_start.size());
+    if (r.lag != 0 || want <= 1 || rows < 2) return {0, T};
+    const int B = std::min(want, rows);
+    std::vector<int> t0{0};
+    for (int b = 1; b < B; ++b) {
+        const int cut = row_start[size_t(b) * rows / B];
+        if (cut > t0.back()) t0.push_back(cut);
+    }
+    t0.push_back(T);
+    return t0;
+}
+
+}  // namespace
+
 int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames,
                              int64_t row_pitch, float* hr, double* residuals, float* pupils_out, int* lag_used) {
     return guarded([&] {
@@ -822,34 +859,99 @@ int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* re
         std::vector<int> ki;
         std::vector<double> kd;
         std::vector<float> kf;
-        if (!same_request(*ctx, *req, ki, kd, kf)) {
-            auto p = std::make_unique<fpmgpu_plan>();
-            p->ctx = ctx;
-            build_plan(*p, *req);
-            if (ctx->cached) delete ctx->cached;
-            ctx->cached = p.release();
+        const std::vector<int> t0 = host_bands(*req);
+        const int B = int(t0.size()) - 1;
+        const bool hit = same_request(*ctx, *req, ki, kd, kf) && ctx->band_t0 == t0;
+        if (!hit) {
+            for (auto* q : ctx->cached) delete q;
+            ctx->cached.clear();
+            ctx->band_t0.clear();
+            for (int b = 0; b < B; ++b) {
+                // band b: the same request over tiles [t0[b], t0[b+1])
+                fpmgpu_recon_request rb = *req;
+                const int a = t0[b], cnt = t0[b + 1] - t0[b];
+                rb.num_tiles = cnt;
+                rb.tile_xy = req->tile_xy + 2 * size_t(a);
+                rb.offsets = req->offsets + 2 * size_t(a) * req->num_leds;
+                if (req->tile_defocus_um) rb.tile_defocus_um = req->tile_defocus_um + a;
+                if (req->pupils) rb.pupils = req->pupils + 2 * size_t(a) * req->cfg.tile_size * req->cfg.tile_size;
+                auto p = std::make_unique<fpmgpu_plan>();
+                p->ctx = ctx;
+                build_plan(*p, rb);
+                ctx->cached.push_back(p.release());
+            }
+            ctx->band_t0 = t0;
             ctx->cached_key_i.swap(ki);
             ctx->cached_key_d.swap(kd);
             ctx->cached_key_f.swap(kf);
         }
-        fpmgpu_plan& p = *ctx->cached;
-        const int W = req->width, H = req->height, F = req->num_frames;
+        while (int(ctx->band_streams.size()) < B) {
+            cudaStream_t bs;
+            cudaEvent_t be;
+            ck(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking), "stream");
+            ck(cudaEventCreateWithFlags(&be, cudaEventDisableTiming), "event");
+            ctx->band_streams.push_back(bs);
+            ctx->band_events.push_back(be);
+        }
+        const fpmgpu_plan& p0 = *ctx->cached[0];
+        const int W = req->width, H = req->height, F = req->num_frames, T = req->num_tiles;
+        const int n = p0.n, N = p0.N, iters = req->iters;
         const int64_t pitch = (int64_t(W) + 63) / 64 * 64;
         uint16_t* fd = ctx->frames.ensure(size_t(F) * H * pitch);
-        ck(cudaMemcpy2DAsync(fd, size_t(pitch) * 2, frames, size_t(row_pitch) * 2, size_t(W) * 2, size_t(F) * H,
-                             cudaMemcpyHostToDevice, s), "frames H2D");
-        const size_t hr_n = size_t(p.T) * p.N * p.N, pup_n = size_t(p.T) * p.n * p.n;
+        const size_t hr_n = size_t(T) * N * N, pup_n = size_t(T) * n * n;
         float2* hr_d = hr ? ctx->hr.ensure(hr_n) : nullptr;
-        double* res_d = ctx->resid.ensure(size_t(p.T) * req->iters);
+        double* res_d = ctx->resid.ensure(size_t(T) * iters);
         float2* pup_d = pupils_out ? ctx->pup.ensure(pup_n) : nullptr;
-        execute_plan(p, fd, pitch, reinterpret_cast<float*>(hr_d), res_d, reinterpret_cast<float*>(pup_d), s);
-        if (hr) ck(cudaMemcpyAsync(hr, hr_d, hr_n * sizeof(float2), cudaMemcpyDeviceToHost, s), "hr D2H");
-        if (residuals)
-            ck(cudaMemcpyAsync(residuals, res_d, sizeof(double) * size_t(p.T) * req->iters, cudaMemcpyDeviceToHost, s),
-               "residual D2H");
-        if (pupils_out) ck(cudaMemcpyAsync(pupils_out, pup_d, pup_n * sizeof(float2), cudaMemcpyDeviceToHost, s), "pupil D2H");
+        ctx->twiddle_table(N);  // its one-time upload must precede the band events on s
+        // frame rows [lo, hi) of every frame: one pitched 3-D copy (x bytes, rows, frames)
+        auto copy_rows = [&](int lo, int hi) {
+            if (hi <= lo) return;
+            cudaMemcpy3DParms m{};
+            m.srcPtr = make_cudaPitchedPtr(const_cast<uint16_t*>(frames), size_t(row_pitch) * 2, size_t(W) * 2, H);
+            m.dstPtr = make_cudaPitchedPtr(fd, size_t(pitch) * 2, size_t(W) * 2, H);
+            m.srcPos = make_cudaPos(0, size_t(lo), 0);
+            m.dstPos = make_cudaPos(0, size_t(lo), 0);
+            m.extent = make_cudaExtent(size_t(W) * 2, size_t(hi - lo), size_t(F));
+            m.kind = cudaMemcpyHostToDevice;
+            ck(cudaMemcpy3DAsync(&m, s), "frames H2D");
+        };
+        int clo = 0, chi = 0;  // rows already on the device: [clo, chi)
+        for (int b = 0; b < B; ++b) {
+            int y0 = H, y1 = 0;
+            for (int t = t0[b]; t < t0[b + 1]; ++t) {
+                y0 = std::min(y0, req->tile_xy[2 * t + 1]);
+                y1 = std::max(y1, req->tile_xy[2 * t + 1] + n);
+            }
+            if (chi <= clo) {
+                copy_rows(y0, y1);
+                clo = y0;
+                chi = y1;
+            } else {
+                copy_rows(std::min(y0, clo), clo);
+                copy_rows(chi, std::max(y1, chi));
+                clo = std::min(y0, clo);
+                chi = std::max(y1, chi);
+            }
+            cudaStream_t bs = ctx->band_streams[b];
+            ck(cudaEventRecord(ctx->band_events[b], s), "event");
+            ck(cudaStreamWaitEvent(bs, ctx->band_events[b], 0), "wait");
+            fpmgpu_plan& pb = *ctx->cached[b];
+            const size_t a = size_t(t0[b]), cnt = size_t(t0[b + 1] - t0[b]);
+            execute_plan(pb, fd, pitch, hr_d ? reinterpret_cast<float*>(hr_d + a * N * N) : nullptr, res_d + a * iters,
+                         pup_d ? reinterpret_cast<float*>(pup_d + a * n * n) : nullptr, bs);
+            if (hr)
+                ck(cudaMemcpyAsync(hr + 2 * a * N * N, hr_d + a * N * N, cnt * N * N * sizeof(float2),
+                                   cudaMemcpyDeviceToHost, bs), "hr D2H");
+            if (residuals)
+                ck(cudaMemcpyAsync(residuals + a * iters, res_d + a * iters, sizeof(double) * cnt * iters,
+                                   cudaMemcpyDeviceToHost, bs), "residual D2H");
+            if (pupils_out)
+                ck(cudaMemcpyAsync(pupils_out + 2 * a * n * n, pup_d + a * n * n, cnt * n * n * sizeof(float2),
+                                   cudaMemcpyDeviceToHost, bs), "pupil D2H");
+        }
+        for (int b = 0; b < B; ++b) ck(cudaStreamSynchronize(ctx->band_streams[b]), "reconstruct");
         ck(cudaStreamSynchronize(s), "reconstruct");
-        if (lag_used) *lag_used = p.lag;
+        if (lag_used) *lag_used = p0.lag;
     });
 }
 

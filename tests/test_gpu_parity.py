@@ -288,3 +288,26 @@ def test_box_kernel_agrees_with_lattice_kernel_n64(eng, monkeypatch):
     b = fpm.run_offline(fs, cfg, seq, opt, engine=fpm.Engine(0), stitch=False)
     for i in range(4):
         assert rel_l2(b.tiles[i], a.tiles[i]) < 1e-5
+
+
+@pytest.mark.parametrize("bands", ["3", "16"])
+def test_banded_host_path_bit_identical(eng, monkeypatch, bands):
+    """The host path's row-band pipeline (H2D of band b+1 under the compute of
+    band b) changes only the schedule: tiles, residuals and pupils are
+    bit-identical to one unbanded launch."""
+    cfg = gpu_cfg(led_scan_rows=7, led_scan_cols=7, tile_overlap=8)
+    fs, _, seq, _ = dataset(cfg, fov=232, seed=34)
+    specs = fpm.partition_tiles(fs.width(), fs.height(), cfg)
+    rng = np.random.default_rng(3)
+    opt = fpm.RunOptions(iters=2, mode="epry", tile_defocus_um=list(rng.uniform(-8, 8, len(specs))))
+    monkeypatch.setenv("FPM_B200_BANDS", "1")
+    a = fpm.run_offline(fs, cfg, seq, opt, engine=eng, stitch=False)
+    monkeypatch.setenv("FPM_B200_BANDS", bands)
+    b = fpm.run_offline(fs, cfg, seq, opt, engine=eng, stitch=False)
+    assert len(specs) == 16
+    assert np.array_equal(a.tiles, b.tiles)
+    assert np.array_equal(np.array([m.pass_mean_residual for m in a.tile_metrics]),
+                          np.array([m.pass_mean_residual for m in b.tile_metrics]))
+    assert a.pupils is not None
+    for pa, pb in zip(a.pupils, b.pupils):
+        assert np.array_equal(pa, pb)
