@@ -188,7 +188,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
     b += 64 * sizeof(float4);                                     // W64 table (+ swizzled copy)
     b += size_t(iters) * sizeof(double);                          // stage sums
     b += size_t(G) * (sizeof(uint64_t) + 16 * sizeof(float));     // mbarriers + reductions
-    b += size_t(L) * (sizeof(short2) + sizeof(int) + 1);          // origins + frame map + bright flags
+    b += size_t(L) * (sizeof(short2) + sizeof(int) + sizeof(float) + 1);  // origins, frame map, sum(I), bright flags
     return b;
 }
 
@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
     off += size_t(L) * sizeof(short2);
     int* F_s = reinterpret_cast<int*>(smem + off);
     off += size_t(L) * sizeof(int);
+    float* D_s = reinterpret_cast<float*>(smem + off);  // sum(I) per LED, formed on its first visit
+    off += size_t(L) * sizeof(float);
     uint8_t* B_s = smem + off;
     uint64_t* bar = bars + g;
     float* rg = red + g * 16;
@@ -234,6 +236,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
     float2* pupil_g = args.pupils + size_t(tile) * 64 * 64;
     const int2 txy = args.tile_xy[tile];
     const float sgn = ((tr + tc) & 1) ? -1.f : 1.f;  // checkerboard (-1)^(i+j), constant per thread
+    const float sgn_eps = sgn * 0x1p-60f;            // see the modulus replacement
 
     // ---- one-time setup: support mask, lattice pupil, tables, W64 table
     uint32_t mask = 0;
@@ -277,6 +280,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
     const float inv_n2 = 1.0f / 4096.0f;  // ifft2's 1/(rows*cols) (field.cpp:64-66)
     uint32_t phase = 0;
     bool issued = false;
+    bool pupil_dirty = true;  // EPRY: max|P|^2 changes only after a pupil step
     auto issue = [&](int2 e) {
         if (MEAS == kMeasTMA && tl == 0) {
             mbar_expect_tx(bar, kIBytes);
@@ -303,28 +307,31 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                 for (int j = 0; j < 4; ++j) v[a][j] = make_float2(0.f, 0.f);
 #pragma unroll
             for (int q = 0; q < NP; ++q) v[Lat::a(q)][Lat::j(q)] = cv[Lat::a(q) * 8 * N + 16 * Lat::j(q)];
-            float omax = 0.f, pmax = 0.f;
+            // EPRY maxima (block-uniform branches): max|O_D|^2 only for bright-field updates (the
+            // only ones that take a pupil step), max|P|^2 only after the pupil changed — otherwise
+            // the reduction slots keep their last values
+            const bool bright = MODE == kModeEPRY && B_s[e.y];
+            if (bright) {
+                float omax = 0.f;
+#pragma unroll
+                for (int q = 0; q < NP; ++q)
+                    omax = fmaxf(omax, ((mask >> q) & 1u) ? cabs2(v[Lat::a(q)][Lat::j(q)]) : 0.f);
+#pragma unroll
+                for (int sh = 16; sh; sh >>= 1) omax = fmaxf(omax, __shfl_xor_sync(kFull, omax, sh));
+                if ((tl & 31) == 0) rg[8 + warp] = omax;
+            }
+            if (MODE == kModeEPRY && pupil_dirty) {
+                float pmax = 0.f;
+#pragma unroll
+                for (int q = 0; q < NP; ++q) pmax = fmaxf(pmax, cabs2(P_s[q * kGroupThreads + tl]));
+#pragma unroll
+                for (int sh = 16; sh; sh >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(kFull, pmax, sh));
+                if ((tl & 31) == 0) rg[12 + warp] = pmax;
+            }
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
-                const float2 O = v[Lat::a(q)][Lat::j(q)];
-                const float2 P = P_s[q * kGroupThreads + tl];
-                if (MODE == kModeEPRY) {
-                    omax = fmaxf(omax, ((mask >> q) & 1u) ? cabs2(O) : 0.f);
-                    pmax = fmaxf(pmax, cabs2(P));
-                }
-                const float2 c = cmul(O, P);
+                const float2 c = cmul(v[Lat::a(q)][Lat::j(q)], P_s[q * kGroupThreads + tl]);
                 v[Lat::a(q)][Lat::j(q)] = make_float2(c.x, -c.y);  // conj: the IFFT runs as conj(FFT(conj x))
-            }
-            if (MODE == kModeEPRY) {
-#pragma unroll
-                for (int sh = 16; sh; sh >>= 1) {
-                    omax = fmaxf(omax, __shfl_xor_sync(kFull, omax, sh));
-                    pmax = fmaxf(pmax, __shfl_xor_sync(kFull, pmax, sh));
-                }
-                if ((tl & 31) == 0) {
-                    rg[8 + warp] = omax;
-                    rg[12 + warp] = pmax;
-                }
             }
 
             // ---- pass 0: centered inverse transform (unscaled; 1/n^2 enters only the residual),
@@ -343,6 +350,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                 mbar_wait(bar, phase);
                 phase ^= 1u;
             }
+            const bool first = e.x == 0;  // sum(I) of this LED's crop is formed once, on its first visit
             float num = 0.f, den_f = 0.f;
             uint32_t den_u = 0;
 #pragma unroll
@@ -354,29 +362,32 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                     if (MEAS == kMeasTMA) {
                         // 128B swizzle: 16-byte chunk b of row i sits at chunk b ^ (i & 7), i & 7 == tr
                         const uint32_t Iu = I_s[(tr + 8 * a) * 64 + ((b ^ tr) << 3) + tc];
-                        den_u += Iu;
+                        if (first) den_u += Iu;
                         Iv = float(Iu);
                     } else {
                         Iv = args.meas_f32[(tr + 8 * a) * 64 + tc + 8 * b];
-                        den_f += Iv;
+                        if (first) den_f += Iv;
                     }
-                    // branch-free: |e|^2 at or below FLT_MIN counts as |e| = 0 (recon.cpp:122)
+                    // branch-free |e| = 0 rule (recon.cpp:122): nudging Re by sgn 2^-60 leaves every
+                    // value with |Re| >= 2^-35 bit-identical and maps e = 0 to (sgn 2^-60, 0), whose
+                    // replacement is exactly the checkerboarded sqrt(I) + 0i
                     const float meas = sqrt_ftz(Iv);
                     const float2 uu = v[a][u];
-                    const float m2 = cabs2(uu);
-                    const bool nz = m2 > kTiny;
+                    const float ux = uu.x + sgn_eps;
+                    const float m2 = fmaf(ux, ux, uu.y * uu.y);
                     const float r = rsqrt_ftz(fmaxf(m2, kTiny));
                     const float dm = fmaf(m2 * r, inv_n2, -meas);  // |e| - sqrt(I)
                     num = fmaf(dm, dm, num);
-                    const float sc = nz ? meas * r : 0.f;
-                    // uu = conj(e n^2): undo the conjugation; the zero case becomes sqrt(I) + 0i
-                    v[a][u] = make_float2(fmaf(uu.x, sc, nz ? 0.f : sgn * meas), -uu.y * sc);
+                    const float sc = meas * r;
+                    // uu = conj(e n^2): undo the conjugation
+                    v[a][u] = make_float2(ux * sc, -uu.y * sc);
                 }
             float den = MEAS == kMeasTMA ? float(den_u) : den_f;
 #pragma unroll
-            for (int sh = 16; sh; sh >>= 1) {
-                num += __shfl_xor_sync(kFull, num, sh);
-                den += __shfl_xor_sync(kFull, den, sh);
+            for (int sh = 16; sh; sh >>= 1) num += __shfl_xor_sync(kFull, num, sh);
+            if (first) {
+#pragma unroll
+                for (int sh = 16; sh; sh >>= 1) den += __shfl_xor_sync(kFull, den, sh);
             }
             if ((tl & 31) == 0) {
                 rg[warp] = num;
@@ -394,13 +405,19 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
             }
             if (tl == 0) {
                 const float nsum = (rg[0] + rg[1]) + (rg[2] + rg[3]);
-                const float dsum = (rg[4] + rg[5]) + (rg[6] + rg[7]);
+                float dsum;
+                if (first) {
+                    dsum = (rg[4] + rg[5]) + (rg[6] + rg[7]);
+                    D_s[e.y] = dsum;
+                } else {
+                    dsum = D_s[e.y];
+                }
                 stage_sum[e.x] += dsum > 0.f ? double(nsum) / double(dsum) : 0.0;
             }
             if (MODE == kModeEPRY) {
                 const float om = fmaxf(fmaxf(rg[8], rg[9]), fmaxf(rg[10], rg[11]));
                 const float pm = fmaxf(fmaxf(rg[12], rg[13]), fmaxf(rg[14], rg[15]));
-                inv_omax = (om > 0.f && B_s[e.y]) ? args.beta / om : 0.f;  // bright-field pupil steps only
+                inv_omax = (om > 0.f && bright) ? args.beta / om : 0.f;  // bright-field pupil steps only
                 inv_pmax = pm > 0.f ? args.alpha / pm : 0.f;
             }
             }
@@ -413,6 +430,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                         cv[Lat::a(q) * 8 * N + 16 * Lat::j(q)] = cmulc(v[Lat::a(q)][Lat::j(q)], P_s[q * kGroupThreads + tl]);
             } else {
                 const bool upd_o = inv_pmax > 0.f, upd_p = inv_omax > 0.f;
+                pupil_dirty = upd_p;
 #pragma unroll
                 for (int c0 = 0; c0 < NP; c0 += 8) {
                     float2 Ov[8];
