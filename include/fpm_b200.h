@@ -126,6 +126,22 @@ int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* re
                              const uint16_t* frames, int64_t row_pitch, float* hr,
                              double* residuals, float* pupils_out, int* lag_used);
 
+/* Online session — replaces run_online (parallel.cpp:198-317): frames arrive one
+ * at a time; each is copied to the device on arrival, and the first-pass
+ * update of sequence position k is launched for every tile as soon as frames
+ * seq_frame[0..k] and the seed frame (init_frame) are resident (updates wait for
+ * the seed, parallel.cpp:266-273). finish() runs the remaining iters-1 passes
+ * (parallel.cpp:289-303) and canvas_to_field. The update order per tile is the
+ * sequential one, so results equal fpmgpu_reconstruct_tiles with lag = 0.
+ * `frame` is a host pointer to one u16 frame [H][row_pitch]; it must stay valid
+ * (and unchanged) until finish returns. Requires lag = 0. */
+typedef struct fpmgpu_online fpmgpu_online;
+int fpmgpu_online_begin(fpmgpu_context* ctx, const fpmgpu_recon_request* req, fpmgpu_online** out);
+int fpmgpu_online_push(fpmgpu_online* on, int frame_index, const uint16_t* frame, int64_t row_pitch,
+                       int* positions_applied);
+int fpmgpu_online_finish(fpmgpu_online* on, float* hr, double* residuals, float* pupils_out);
+int fpmgpu_online_destroy(fpmgpu_online* on);
+
 /* Plans: validate + upload the geometry tables once, then execute on device
  * buffers (frames/hr/residuals/pupils_out are DEVICE pointers; row_pitch in
  * elements, row_pitch*2 must be a multiple of 16 bytes). `stream` is a

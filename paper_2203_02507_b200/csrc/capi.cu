@@ -352,22 +352,18 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     p.req.pupils = nullptr;
 }
 
-void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* hr, double* resid,
-                  float* pupils_out, cudaStream_t s) {
+// pupils (build_pupil per tile, or the caller's) + init_canvas: bilinear(sqrt(seed crop)) ->
+// centered FFT N x N -> / up^2 (recon.cpp:61-86)
+void plan_prologue(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, cudaStream_t s) {
     const fpmgpu_recon_request& r = p.req;
-    const CUtensorMap map = encode_frames_map(frames, p.F, r.height, r.width, pitch);
-    cudaEvent_t* ev = p.slot_events();
-    if (ev) ck(cudaEventRecord(ev[0], s), "event");
     const double dk = 1.0 / (p.n * dx_obj(r.cfg));
     const double inv_l2 = 1.0 / (r.cfg.wavelength * r.cfg.wavelength);
-    // pupils (build_pupil per tile, or the caller's)
     if (p.has_pupils)
         ck(cudaMemcpyAsync(p.pupils.p, p.pupils_init.p, sizeof(float2) * size_t(p.T) * p.n * p.n,
                            cudaMemcpyDeviceToDevice, s), "pupil copy");
     else
         ck(fpmk::launch_build_pupils(p.pupils.p, p.support.p, p.has_defocus ? p.defocus.p : nullptr, p.n, p.T, dk,
                                      inv_l2, s), "build_pupils");
-    // init_canvas: bilinear(sqrt(seed crop)) -> centered FFT N x N -> / up^2
     fpmk::LinesArgs la{};
     la.tw = p.ctx->twiddle_table(p.N);
     la.frame = frames + size_t(r.init_frame) * size_t(r.height) * size_t(pitch);
@@ -381,8 +377,13 @@ void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* 
     ck(fpmk::launch_lines(0, p.N, la, p.T, s), "init rows");
     la.scale = float(1.0 / (double(r.cfg.upsample) * r.cfg.upsample));
     ck(fpmk::launch_lines(1, p.N, la, p.T, s), "init cols");
-    if (ev) ck(cudaEventRecord(ev[1], s), "event");
-    // the LED loop
+}
+
+// the LED loop over schedule slots [s0, s1); residuals of the touched stages are
+// stored (acc = false) or added (acc = true)
+void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* resid, int s0, int s1, bool acc,
+               cudaStream_t s) {
+    const fpmgpu_recon_request& r = p.req;
     fpmk::LoopArgs a{};
     a.canvas = p.canvas.p;
     a.pupils = p.pupils.p;
@@ -393,7 +394,9 @@ void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* 
     a.tile_xy = p.tile_xy.p;
     a.residuals = resid ? resid : p.resid.p;
     a.slots = p.G > 1 ? p.slots.p : nullptr;
-    a.num_slots = p.num_slots;
+    a.slot_begin = s0;
+    a.num_slots = s1;
+    a.resid_accumulate = acc ? 1 : 0;
     a.T = p.T;
     a.L = p.L;
     a.iters = r.iters;
@@ -411,10 +414,19 @@ void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* 
         bx.b0 = p.b0;
         ck(fpmk::launch_loop_box(p.n, r.mode, a, bx, p.T, s), "LED loop (box)");
     } else {
+        const CUtensorMap map = encode_frames_map(frames, p.F, r.height, r.width, pitch);
         ck(fpmk::launch_loop64(r.mode, p.prune, fpmk::kMeasTMA, p.G, &map, a, p.T, s), "LED loop");
     }
-    if (ev) ck(cudaEventRecord(ev[2], s), "event");
-    // canvas_to_field: centered IFFT N x N * up^2 (the 1/N^2 of ifft2 folded in)
+}
+
+// canvas_to_field: centered IFFT N x N * up^2 (the 1/N^2 of ifft2 folded in), recon.cpp:88-91
+void plan_epilogue(fpmgpu_plan& p, float* hr, float* pupils_out, cudaStream_t s) {
+    const fpmgpu_recon_request& r = p.req;
+    fpmk::LinesArgs la{};
+    la.tw = p.ctx->twiddle_table(p.N);
+    la.tile_xy = p.tile_xy.p;
+    la.n = p.n;
+    la.up = r.cfg.upsample;
     la.src = p.canvas.p;
     la.dst = p.canvas.p;
     la.scale = 1.0f;
@@ -422,6 +434,21 @@ void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* 
     la.dst = hr ? reinterpret_cast<float2*>(hr) : p.canvas.p;
     la.scale = float(double(r.cfg.upsample) * r.cfg.upsample / (double(p.N) * p.N));
     ck(fpmk::launch_lines(3, p.N, la, p.T, s), "final cols");
+    if (pupils_out)
+        ck(cudaMemcpyAsync(pupils_out, p.pupils.p, sizeof(float2) * size_t(p.T) * p.n * p.n,
+                           cudaMemcpyDeviceToDevice, s), "pupil out");
+}
+
+void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* hr, double* resid,
+                  float* pupils_out, cudaStream_t s) {
+    cudaEvent_t* ev = p.slot_events();
+    if (ev) ck(cudaEventRecord(ev[0], s), "event");
+    plan_prologue(p, frames, pitch, s);
+    if (ev) ck(cudaEventRecord(ev[1], s), "event");
+    plan_loop(p, frames, pitch, resid, 0, p.num_slots, false, s);
+    if (ev) ck(cudaEventRecord(ev[2], s), "event");
+    // the pupil copy-out stays outside the finalize phase event
+    plan_epilogue(p, hr, nullptr, s);
     if (ev) ck(cudaEventRecord(ev[3], s), "event");
     if (pupils_out)
         ck(cudaMemcpyAsync(pupils_out, p.pupils.p, sizeof(float2) * size_t(p.T) * p.n * p.n,
@@ -952,6 +979,117 @@ int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* re
         for (int b = 0; b < B; ++b) ck(cudaStreamSynchronize(ctx->band_streams[b]), "reconstruct");
         ck(cudaStreamSynchronize(s), "reconstruct");
         if (lag_used) *lag_used = p0.lag;
+    });
+}
+
+struct fpmgpu_online {
+    fpmgpu_context* ctx = nullptr;
+    std::unique_ptr<fpmgpu_plan> plan;
+    DevBuf<uint16_t> frames;
+    DevBuf<double> resid;
+    int64_t pitch = 0;
+    cudaStream_t copy = nullptr, comp = nullptr;
+    std::vector<cudaEvent_t> arrived;  // per frame: its H2D copy is complete
+    std::vector<uint8_t> present;
+    std::vector<int> seq_frame;  // host copy (the plan keeps no caller pointers)
+    bool seeded = false;
+    int next = 0;  // first sequence position not yet launched
+    ~fpmgpu_online() {
+        if (comp) cudaStreamSynchronize(comp);
+        if (copy) cudaStreamSynchronize(copy);
+        for (auto e : arrived) cudaEventDestroy(e);
+        if (comp) cudaStreamDestroy(comp);
+        if (copy) cudaStreamDestroy(copy);
+    }
+};
+
+int fpmgpu_online_begin(fpmgpu_context* ctx, const fpmgpu_recon_request* req, fpmgpu_online** out) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (req->lag != 0) throw ConfigError("online mode runs the sequential schedule (lag 0)");
+        auto on = std::make_unique<fpmgpu_online>();
+        on->ctx = ctx;
+        on->plan = std::make_unique<fpmgpu_plan>();
+        on->plan->ctx = ctx;
+        build_plan(*on->plan, *req);
+        const fpmgpu_plan& p = *on->plan;
+        on->pitch = (int64_t(req->width) + 63) / 64 * 64;
+        on->frames.ensure(size_t(p.F) * req->height * on->pitch);
+        on->resid.ensure(size_t(p.T) * req->iters);
+        ck(cudaStreamCreateWithFlags(&on->copy, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&on->comp, cudaStreamNonBlocking), "stream");
+        on->arrived.resize(size_t(p.F));
+        for (auto& e : on->arrived) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        on->present.assign(size_t(p.F), 0);
+        on->seq_frame.assign(req->seq_frame, req->seq_frame + p.L);
+        ctx->twiddle_table(p.N);
+        // the plan's table uploads and the twiddles went out on the context stream
+        ck(cudaStreamSynchronize(ctx->stream), "online begin");
+        ck(cudaMemsetAsync(on->resid.p, 0, sizeof(double) * size_t(p.T) * req->iters, on->comp), "residual clear");
+        *out = on.release();
+    });
+}
+
+int fpmgpu_online_push(fpmgpu_online* on, int frame_index, const uint16_t* frame, int64_t row_pitch,
+                       int* positions_applied) {
+    return guarded([&] {
+        ck(cudaSetDevice(on->ctx->device), "cudaSetDevice");
+        fpmgpu_plan& p = *on->plan;
+        const fpmgpu_recon_request& r = p.req;
+        if (frame_index < 0 || frame_index >= p.F) throw DataError("frame index outside the frame set");
+        if (on->present[size_t(frame_index)]) throw DataError("frame pushed twice");
+        uint16_t* dst = on->frames.p + size_t(frame_index) * r.height * on->pitch;
+        ck(cudaMemcpy2DAsync(dst, size_t(on->pitch) * 2, frame, size_t(row_pitch) * 2, size_t(r.width) * 2,
+                             size_t(r.height), cudaMemcpyHostToDevice, on->copy), "frame H2D");
+        ck(cudaEventRecord(on->arrived[size_t(frame_index)], on->copy), "event");
+        on->present[size_t(frame_index)] = 1;
+        if (!on->seeded && on->present[size_t(r.init_frame)]) {
+            ck(cudaStreamWaitEvent(on->comp, on->arrived[size_t(r.init_frame)], 0), "wait");
+            plan_prologue(p, on->frames.p, on->pitch, on->comp);
+            on->seeded = true;
+        }
+        if (on->seeded) {
+            int k = on->next;
+            while (k < p.L && on->present[size_t(on->seq_frame[size_t(k)])]) {
+                ck(cudaStreamWaitEvent(on->comp, on->arrived[size_t(on->seq_frame[size_t(k)])], 0), "wait");
+                ++k;
+            }
+            if (k > on->next) {  // first-pass slots [next, k): stage 0, positions next .. k-1
+                plan_loop(p, on->frames.p, on->pitch, on->resid.p, on->next, k, true, on->comp);
+                on->next = k;
+            }
+        }
+        if (positions_applied) *positions_applied = on->next;
+    });
+}
+
+int fpmgpu_online_finish(fpmgpu_online* on, float* hr, double* residuals, float* pupils_out) {
+    return guarded([&] {
+        ck(cudaSetDevice(on->ctx->device), "cudaSetDevice");
+        fpmgpu_plan& p = *on->plan;
+        const fpmgpu_recon_request& r = p.req;
+        if (!on->seeded) throw DataError("missing frame for the canvas seed");
+        if (on->next < p.L) throw DataError("missing frame for a sequence LED");
+        if (r.iters > 1) plan_loop(p, on->frames.p, on->pitch, on->resid.p, p.L, r.iters * p.L, true, on->comp);
+        const size_t hr_n = size_t(p.T) * p.N * p.N, pup_n = size_t(p.T) * p.n * p.n;
+        float2* hr_d = hr ? on->ctx->hr.ensure(hr_n) : nullptr;
+        plan_epilogue(p, reinterpret_cast<float*>(hr_d), nullptr, on->comp);
+        if (hr) ck(cudaMemcpyAsync(hr, hr_d, hr_n * sizeof(float2), cudaMemcpyDeviceToHost, on->comp), "hr D2H");
+        if (residuals)
+            ck(cudaMemcpyAsync(residuals, on->resid.p, sizeof(double) * size_t(p.T) * r.iters,
+                               cudaMemcpyDeviceToHost, on->comp), "residual D2H");
+        if (pupils_out)
+            ck(cudaMemcpyAsync(pupils_out, p.pupils.p, pup_n * sizeof(float2), cudaMemcpyDeviceToHost, on->comp),
+               "pupil D2H");
+        ck(cudaStreamSynchronize(on->comp), "online finish");
+    });
+}
+
+int fpmgpu_online_destroy(fpmgpu_online* on) {
+    return guarded([&] {
+        if (!on) return;
+        cudaSetDevice(on->ctx->device);
+        delete on;
     });
 }
 

@@ -37,6 +37,9 @@ constexpr int kIBytes = 64 * 64 * 2;            // staged u16 measurement, TMA 1
 constexpr int kTBytes = 64 * 64 * 8;            // transpose buffer (swizzled, unpadded)
 constexpr int kGroupBytes = kIBytes + kTBytes;  // 40 KB, a multiple of 1 KB
 constexpr int kGroupThreads = 128;
+#ifndef FPM_LOOP_MINB
+#define FPM_LOOP_MINB 4  // resident tiles per SM the register budget is sized for
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -193,7 +196,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
 }
 
 template <int MODE, bool PRUNE, int MEAS, int G, int N>
-__global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
+__global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     fpm_loop64(const __grid_constant__ CUtensorMap tmap, const LoopArgs args) {
     using Lat = Lattice<PRUNE>;
     constexpr int NP = Lat::NP;
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
     // canvas offset of lattice position (a, j) relative to the sub-aperture origin
     const int cbase = tr * N + tc + 8 * h;
 
-    for (int s = 0; s < args.num_slots; ++s) {
+    for (int s = args.slot_begin; s < args.num_slots; ++s) {
         const int2 e = slot_entry<G>(args, s, g);
         if (e.x >= 0) {
             if (!issued) issue(e);
@@ -350,7 +353,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
                 mbar_wait(bar, phase);
                 phase ^= 1u;
             }
-            const bool first = e.x == 0;  // sum(I) of this LED's crop is formed once, on its first visit
+            // sum(I) of an LED's crop is formed once, on its first visit in this launch
+            const bool first = G == 1 ? s - args.slot_begin < L : e.x == 0;
             float num = 0.f, den_f = 0.f;
             uint32_t den_u = 0;
 #pragma unroll
@@ -456,8 +460,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? 4 : 2)
     }
 
     // ---- per-pass mean residual; EPRY pupil back to global
-    for (int k = threadIdx.x; k < args.iters; k += blockDim.x)
-        args.residuals[size_t(tile) * args.iters + k] = stage_sum[k] / double(L);
+    store_residuals(args, tile, stage_sum, G == 1);
     if (MODE == kModeEPRY && g == 0) {
 #pragma unroll
         for (int q = 0; q < NP; ++q)

@@ -24,6 +24,8 @@ struct LoopArgs {
     const float* meas_f32;    // kMeasF32: [n][n] intensities (update_step API)
     const int2* slots;        // G > 1: [num_slots][G] (stage, position), stage < 0 = idle
     int num_slots;            // G == 1: iters * L (implicit slots)
+    int slot_begin;           // run slots [slot_begin, num_slots) (G == 1; 0 for a whole run)
+    int resid_accumulate;     // residuals of the stages touched are added to (online passes)
     int T, L, iters, N, nslots;
     float alpha, beta;        // EPRY step sizes
 };
@@ -53,6 +55,19 @@ size_t box_smem_bytes(int n, int box, int L, int iters, bool scratch_in_smem);
 cudaError_t launch_loop_box(int n, int mode, const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s);
 
 size_t loop_smem_bytes(int G, int nslots, int L, int iters);
+
+#ifdef __CUDACC__
+// Per-pass mean residuals of the stages a launch touched (all of them for a
+// whole run; a stage range for the online passes, accumulated).
+__device__ __forceinline__ void store_residuals(const LoopArgs& a, int tile, const double* stage_sum, bool ranged) {
+    const int k0 = ranged ? a.slot_begin / a.L : 0;
+    const int k1 = ranged ? (a.num_slots - 1) / a.L : a.iters - 1;
+    for (int k = k0 + int(threadIdx.x); k <= k1; k += blockDim.x) {
+        double* r = a.residuals + size_t(tile) * a.iters + k;
+        *r = (a.resid_accumulate ? *r : 0.0) + stage_sum[k] / double(a.L);
+    }
+}
+#endif
 cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorMap* tmap,
                           const LoopArgs& a, int T, cudaStream_t s);
 // which: 0 init rows (frame -> canvas), 1 init cols, 2 finalize rows, 3 finalize cols

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
     const float inv_n2 = 1.0f / float(NLR * NLR);
     __syncthreads();
 
-    for (int s = 0; s < args.num_slots; ++s) {
+    for (int s = args.slot_begin; s < args.num_slots; ++s) {
         const int it = s / L, pos = s % L;
         const short2 o = O_s[pos];
         const float2* cvc = canvas + size_t(o.x) * NC + o.y;
@@ -311,8 +311,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
         }
         __syncthreads();  // canvas, pupil and reductions settled before the next update
     }
-    for (int k = threadIdx.x; k < args.iters; k += blockDim.x)
-        args.residuals[size_t(tile) * args.iters + k] = stage_sum[k] / double(L);
+    store_residuals(args, tile, stage_sum, true);
 }
 
 template <int NLR, int MODE, int NC, bool SMEM_S>

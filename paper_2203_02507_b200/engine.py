@@ -181,6 +181,7 @@ class RunResult:
     timing: TimingRow
     tile_metrics: list
     pupils: np.ndarray | None = None
+    acquisition_s: float = 0.0  # online mode only (parallel.hpp:76)
 
 
 def _p(a, ctype=C.c_int):
@@ -461,16 +462,7 @@ def run_offline(frames: FrameSet, cfg: OpticalConfig, seq, opt: RunOptions, engi
     if opt.workers < 1:
         raise ConfigError("workers must be >= 1")
     t0 = time.perf_counter()
-    specs = partition_tiles(frames.width(), frames.height(), cfg, opt.defocus_um)
-    if opt.max_tiles is not None:
-        if opt.max_tiles > len(specs):
-            raise ConfigError("requested tile count exceeds partition")
-        specs = specs[: opt.max_tiles]
-    if opt.tile_defocus_um is not None:
-        if len(opt.tile_defocus_um) != len(specs):
-            raise ConfigError("tile_defocus_um must list one value per tile")
-        for s, z in zip(specs, opt.tile_defocus_um):
-            s.defocus_um = float(z)
+    specs = select_tiles(frames, cfg, opt)
     pipeline = opt.force_pipeline or opt.workers > len(specs)
     lag = 0
     if pipeline:
@@ -487,6 +479,83 @@ def run_offline(frames: FrameSet, cfg: OpticalConfig, seq, opt: RunOptions, engi
     timing = TimingRow("", "offline", opt.workers, 1 if opt.lag is None else opt.lag, len(specs), opt.iters,
                        wall, wall / max(len(specs), 1))
     return RunResult(specs, hr, stitched, timing, [ReconMetrics(r.tolist(), 0.0) for r in res], pup)
+
+
+def select_tiles(frames: FrameSet, cfg: OpticalConfig, opt: RunOptions) -> list:
+    """select_tiles (parallel.cpp:142-153) plus the per-tile defocus extension."""
+    specs = partition_tiles(frames.width(), frames.height(), cfg, opt.defocus_um)
+    if opt.max_tiles is not None:
+        if opt.max_tiles > len(specs):
+            raise ConfigError("requested tile count exceeds partition")
+        specs = specs[: opt.max_tiles]
+    if opt.tile_defocus_um is not None:
+        if len(opt.tile_defocus_um) != len(specs):
+            raise ConfigError("tile_defocus_um must list one value per tile")
+        for s, z in zip(specs, opt.tile_defocus_um):
+            s.defocus_um = float(z)
+    return specs
+
+
+def run_online(frames: FrameSet, cfg: OpticalConfig, seq, opt: RunOptions, delay_scale: float = 1.0,
+               engine: Engine | None = None, stitch: bool = True) -> RunResult:
+    """run_online (parallel.cpp:198-317): frames are replayed against their
+    timestamps (scaled by delay_scale); each arrival is copied to the device and
+    the first-pass update of every newly complete sequence position runs on all
+    tiles at once (fpmgpu_online_push), waiting for the on-axis seed like the
+    reference (parallel.cpp:266-273); the remaining iters-1 passes, the HR
+    fields and the mosaic follow the stream (parallel.cpp:289-305). Same update
+    order as run_offline, hence the same tiles."""
+    if opt.workers < 1:
+        raise ConfigError("workers must be >= 1")
+    if delay_scale < 0:
+        raise ConfigError("delay scale must be >= 0")
+    t0 = time.perf_counter()
+    specs = select_tiles(frames, cfg, opt)
+    stream = []
+    for led in seq:
+        f = frames.find(led)
+        if f is None:
+            raise DataError("missing frame for a sequence LED")
+        stream.append(f)
+    req = make_request(frames, cfg, seq, specs, opt.iters, mode=opt.mode, alpha=opt.alpha, beta=opt.beta)
+    eng = engine or default_engine()
+    r, keep = req.c()
+    imgs = np.ascontiguousarray(frames.images, np.uint16)
+    ts = (np.zeros(len(frames.leds)) if frames.timestamps is None or len(frames.timestamps) == 0
+          else np.asarray(frames.timestamps, np.float64))
+    T, n, N = len(specs), cfg.tile_size, cfg.hr_size()
+    hr = np.zeros((T, N, N), np.complex64)
+    res = np.zeros((T, opt.iters), np.float64)
+    pup = np.zeros((T, n, n), np.complex64)
+    h = C.c_void_p()
+    check(lib().fpmgpu_online_begin(eng.handle, C.byref(r), C.byref(h)))
+    try:
+        applied = C.c_int()
+        pushed = set()
+        frame_bytes = imgs.shape[1] * imgs.shape[2] * 2
+        for f in stream:  # the ordered frame source (parallel.cpp:220-233)
+            wait = t0 + float(ts[f]) * delay_scale - time.perf_counter()
+            if wait > 0:
+                time.sleep(wait)
+            if f in pushed:
+                continue
+            pushed.add(f)
+            check(lib().fpmgpu_online_push(h, f, imgs.ctypes.data + f * frame_bytes, imgs.shape[2],
+                                           C.byref(applied)))
+        if req.init_frame not in pushed:  # seed outside the sequence: read at stream end
+            check(lib().fpmgpu_online_push(h, req.init_frame, imgs.ctypes.data + req.init_frame * frame_bytes,
+                                           imgs.shape[2], C.byref(applied)))
+        check(lib().fpmgpu_online_finish(h, hr.ctypes.data, res.ctypes.data, pup.ctypes.data))
+    finally:
+        lib().fpmgpu_online_destroy(h)
+        del keep
+    acquisition = float(ts[stream[-1]]) * delay_scale if stream else 0.0
+    stitched = None
+    if stitch and opt.max_tiles is None:
+        stitched = stitch_mosaic(hr, specs, cfg, engine)
+    wall = time.perf_counter() - t0
+    timing = TimingRow("", "online", opt.workers, 1, T, opt.iters, wall, wall / max(T, 1))
+    return RunResult(specs, hr, stitched, timing, [ReconMetrics(x.tolist(), 0.0) for x in res], pup, acquisition)
 
 
 def stitch_mosaic(tiles: np.ndarray, specs: list, cfg: OpticalConfig, engine: Engine | None = None) -> np.ndarray:

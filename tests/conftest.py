@@ -18,3 +18,11 @@ def orc():
     from oracle import oracle
     oracle.lib()
     return oracle
+
+
+@pytest.fixture(scope="session")
+def eng():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2203_02507_b200 as fpm
+    return fpm.default_engine(0)

@@ -16,13 +16,6 @@ PER_ITER_TOL = 1e-4
 FINAL_TOL = 1e-3
 
 
-@pytest.fixture(scope="module")
-def eng():
-    import torch
-    assert torch.cuda.is_available(), "GPU tests need a B200"
-    return fpm.default_engine(0)
-
-
 def test_init_canvas_and_finalize(orc, eng):
     cfg = gpu_cfg()
     fs, ofs, seq, _ = dataset(cfg, seed=2)

@@ -1,0 +1,65 @@
+"""run_online (parallel.cpp:198-317) on the device: the streaming session
+(fpmgpu_online_*) must reproduce run_offline bit for bit — the reference's own
+test "online replay converges to the offline result" (test_parallel.cpp:202-216)
+requires max_abs_diff == 0 — and keep its acquisition / timing bookkeeping."""
+import numpy as np
+import pytest
+
+import paper_2203_02507_b200 as fpm
+from tests.helpers import dataset, gpu_cfg
+
+
+def test_online_rejects_bad_arguments_on_cpu():
+    cfg = gpu_cfg()
+    fs = fpm.FrameSet(np.zeros((1, 64, 64), np.uint16), [(0, 0)], np.zeros(1))
+    with pytest.raises(fpm.ConfigError, match="delay scale must be >= 0"):
+        fpm.run_online(fs, cfg, [(0, 0)], fpm.RunOptions(iters=1), delay_scale=-1.0)
+    with pytest.raises(fpm.ConfigError, match="workers must be >= 1"):
+        fpm.run_online(fs, cfg, [(0, 0)], fpm.RunOptions(iters=1, workers=0))
+    with pytest.raises(fpm.DataError, match="missing frame for a sequence LED"):
+        fpm.run_online(fs, cfg, [(0, 0), (1, 1)], fpm.RunOptions(iters=1))
+
+
+@pytest.mark.gpu
+def test_online_replay_equals_offline(eng):
+    """test_parallel.cpp:202-216: toy config, spiral, 2 iterations, 100x replay."""
+    cfg = gpu_cfg()
+    fs, _, seq, _ = dataset(cfg, seed=33)
+    opt = fpm.RunOptions(iters=2, workers=1)
+    off = fpm.run_offline(fs, cfg, seq, opt, engine=eng)
+    on = fpm.run_online(fs, cfg, seq, opt, 0.01, engine=eng)
+    assert on.tiles.shape == off.tiles.shape
+    for a, b in zip(on.tiles, off.tiles):
+        assert np.max(np.abs(a - b)) == 0.0
+    assert on.acquisition_s == pytest.approx(9 * 0.33 * 0.01)
+    assert on.timing.mode == "online"
+    assert np.allclose([m.pass_mean_residual for m in on.tile_metrics],
+                       [m.pass_mean_residual for m in off.tile_metrics], rtol=1e-12)
+
+
+@pytest.mark.gpu
+def test_online_raster_waits_for_seed(eng):
+    """Raster order: the on-axis seed arrives mid-stream; earlier frames are
+    buffered until it does (parallel.cpp:266-273). Multi-tile FOV."""
+    cfg = gpu_cfg(led_scan_rows=5, led_scan_cols=5)
+    fs, _, seq, _ = dataset(cfg, order="raster", fov=120, seed=35)
+    assert seq[0] != cfg.center_led
+    opt = fpm.RunOptions(iters=3)
+    off = fpm.run_offline(fs, cfg, seq, opt, engine=eng)
+    on = fpm.run_online(fs, cfg, seq, opt, 0.0, engine=eng)
+    assert np.array_equal(on.tiles, off.tiles)
+    assert np.array_equal(on.stitched, off.stitched)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [64, 128])
+def test_online_epry_equals_offline(eng, n):
+    """The EPRY extension and the general-n kernel through the streaming path."""
+    cfg = fpm.OpticalConfig(tile_size=n, tile_overlap=8, upsample=4, led_scan_rows=7, led_scan_cols=7)
+    fs, _, seq, _ = dataset(cfg, fov=2 * n - 8 if n == 64 else n, seed=36, defocus_um=8.0)
+    T = len(fpm.partition_tiles(fs.width(), fs.height(), cfg))
+    opt = fpm.RunOptions(iters=2, mode="epry", tile_defocus_um=[5.0] * T)
+    off = fpm.run_offline(fs, cfg, seq, opt, engine=eng, stitch=False)
+    on = fpm.run_online(fs, cfg, seq, opt, 0.0, engine=eng, stitch=False)
+    assert np.array_equal(on.tiles, off.tiles)
+    assert np.array_equal(on.pupils, off.pupils)
