@@ -11,6 +11,7 @@
 // (device from $FPM_B200_DEVICE, default 0), created on first use.
 #pragma once
 
+#include <chrono>
 #include <complex>
 #include <cstdint>
 #include <cstdio>
@@ -21,6 +22,7 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -649,6 +651,96 @@ inline RunResult run_offline(const FrameSet& frames, const OpticalConfig& cfg, c
     res.timing.lag = opt.lag.value_or(1);
     res.timing.tiles = int(res.specs.size());
     res.timing.iters = opt.iters;
+    return res;
+}
+
+// run_online (parallel.cpp:198-317): frames replayed against their timestamps
+// (x delay_scale); each arrival goes to the device and the first-pass update
+// of every newly complete sequence position runs on all tiles
+// (fpmgpu_online_push); the remaining passes, HR fields and mosaic follow.
+inline RunResult run_online(const FrameSet& frames, const OpticalConfig& cfg, const LedSequence& seq,
+                            const RunOptions& opt, double delay_scale = 1.0) {
+    if (opt.workers < 1) throw ConfigError("workers must be >= 1");
+    if (delay_scale < 0) throw ConfigError("delay scale must be >= 0");
+    const auto t0 = std::chrono::steady_clock::now();
+    RunResult res;
+    res.specs = partition_tiles(frames.width(), frames.height(), cfg, opt.defocus_um);
+    if (opt.max_tiles) {
+        if (*opt.max_tiles > int(res.specs.size())) throw ConfigError("requested tile count exceeds partition");
+        res.specs.resize(size_t(*opt.max_tiles));
+    }
+    if (!opt.tile_defocus_um.empty()) {
+        if (opt.tile_defocus_um.size() != res.specs.size())
+            throw ConfigError("tile_defocus_um must list one value per tile");
+        for (size_t i = 0; i < res.specs.size(); ++i) res.specs[i].defocus_um = opt.tile_defocus_um[i];
+    }
+    std::vector<int> stream;
+    for (const auto& led : seq) {
+        int idx = -1;
+        for (size_t f = 0; f < frames.frames.size() && idx < 0; ++f)
+            if (frames.frames[f].led == led) idx = int(f);
+        if (idx < 0) throw DataError("missing frame for a sequence LED");
+        stream.push_back(idx);
+    }
+    detail::Batch b = detail::make_batch(frames, res.specs, cfg, seq);
+    const std::vector<uint16_t> px = detail::pack_frames(frames);
+    fpmgpu_recon_request r{};
+    r.cfg = cfg.c();
+    r.iters = opt.iters;
+    r.mode = opt.mode;
+    r.alpha = opt.alpha;
+    r.beta = opt.beta;
+    r.num_tiles = int(res.specs.size());
+    r.tile_xy = b.xy.data();
+    r.num_leds = int(seq.size());
+    r.offsets = b.offsets.data();
+    r.seq_frame = b.seq_frame.data();
+    r.init_frame = detail::seed_frame(frames, cfg);
+    bool any_defocus = false;
+    for (double z : b.defocus) any_defocus |= z != 0.0;
+    r.tile_defocus_um = any_defocus ? b.defocus.data() : nullptr;
+    r.num_frames = int(frames.frames.size());
+    r.height = frames.height();
+    r.width = frames.width();
+    const size_t N = size_t(cfg.hr_size()), T = res.specs.size();
+    const size_t frame_px = size_t(r.height) * size_t(r.width);
+    std::vector<float> hr(T * N * N * 2);
+    std::vector<double> resid(T * size_t(opt.iters));
+    fpmgpu_online* on = nullptr;
+    detail::check(fpmgpu_online_begin(detail::ctx(), &r, &on));
+    try {
+        std::vector<char> pushed(frames.frames.size(), 0);
+        for (int f : stream) {  // the ordered frame source (parallel.cpp:220-233)
+            std::this_thread::sleep_until(t0 + std::chrono::duration<double>(frames.frames[size_t(f)].timestamp_s *
+                                                                             delay_scale));
+            if (pushed[size_t(f)]) continue;
+            pushed[size_t(f)] = 1;
+            detail::check(fpmgpu_online_push(on, f, px.data() + size_t(f) * frame_px, r.width, nullptr));
+        }
+        if (!pushed[size_t(r.init_frame)])
+            detail::check(fpmgpu_online_push(on, r.init_frame, px.data() + size_t(r.init_frame) * frame_px, r.width,
+                                             nullptr));
+        detail::check(fpmgpu_online_finish(on, hr.data(), resid.data(), nullptr));
+    } catch (...) {
+        fpmgpu_online_destroy(on);
+        throw;
+    }
+    fpmgpu_online_destroy(on);
+    res.acquisition_s = stream.empty() ? 0.0 : frames.frames[size_t(stream.back())].timestamp_s * delay_scale;
+    for (size_t t = 0; t < T; ++t) {
+        res.tiles.push_back(detail::from_c64(hr.data() + t * N * N * 2, long(N), long(N)));
+        ReconMetrics m;
+        m.pass_mean_residual.assign(resid.begin() + long(t) * opt.iters, resid.begin() + long(t + 1) * opt.iters);
+        res.tile_metrics.push_back(m);
+    }
+    if (!opt.max_tiles) res.stitched = stitch_mosaic(res.tiles, res.specs, cfg);
+    res.timing.mode = "online";
+    res.timing.workers = opt.workers;
+    res.timing.lag = 1;
+    res.timing.tiles = int(T);
+    res.timing.iters = opt.iters;
+    res.timing.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    res.timing.per_tile_mean_s = T ? res.timing.wall_s / double(T) : 0.0;
     return res;
 }
 

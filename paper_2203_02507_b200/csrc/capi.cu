@@ -252,8 +252,6 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     if (p.n != 64 && p.n != 128 && p.n != 256)
         throw Unsupported("tile side " + std::to_string(p.n) + " has no device kernel in this build (64/128/256)");
     p.use_box = p.n != 64 || box_forced();
-    if (p.use_box && r.lag != 0)
-        throw Unsupported("the pipelined schedule runs on the n = 64 kernel only in this build");
     if (p.N != 256 && p.N != 512 && p.N != 1024)
         throw Unsupported("canvas side " + std::to_string(p.N) + " has no line-FFT kernel (256/512/1024)");
     for (int t = 0; t < p.T; ++t) {

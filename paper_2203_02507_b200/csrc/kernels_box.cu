@@ -165,8 +165,20 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
     const float inv_n2 = 1.0f / float(NLR * NLR);
     __syncthreads();
 
-    for (int s = args.slot_begin; s < args.num_slots; ++s) {
-        const int it = s / L, pos = s % L;
+    // sequential: slot s = (s / L, s % L); pipelined: the slot's entries run back to back on
+    // the whole CTA — they touch disjoint disks, so any order equals the concurrent one
+    const int G = args.slots ? 2 : 1;
+    for (int e = args.slot_begin * G; e < args.num_slots * G; ++e) {
+        int it, pos;
+        if (G == 1) {
+            it = e / L;
+            pos = e % L;
+        } else {
+            const int2 en = args.slots[e];
+            if (en.x < 0) continue;
+            it = en.x;
+            pos = en.y;
+        }
         const short2 o = O_s[pos];
         const float2* cvc = canvas + size_t(o.x) * NC + o.y;
         float2* cv = canvas + size_t(o.x) * NC + o.y;
@@ -311,7 +323,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
         }
         __syncthreads();  // canvas, pupil and reductions settled before the next update
     }
-    store_residuals(args, tile, stage_sum, true);
+    store_residuals(args, tile, stage_sum, G == 1);
 }
 
 template <int NLR, int MODE, int NC, bool SMEM_S>

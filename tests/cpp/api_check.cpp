@@ -152,6 +152,14 @@ static void gpu_checks(const std::string& dir) {
     RunResult rr = run_offline(fs, cfg, seq, opt);
     CHECK(rr.stitched.rows() == long(fs.height()) * cfg.upsample);
     write_field(dir + "/stitched.bin", rr.stitched);
+    // run_online replays the stream and reproduces run_offline bit for bit (test_parallel.cpp:202-216)
+    RunResult ro = run_online(fs, cfg, seq, opt, 0.0);
+    bool same_on = ro.tiles.size() == rr.tiles.size();
+    for (size_t t = 0; same_on && t < ro.tiles.size(); ++t)
+        for (long i = 0; i < ro.tiles[t].rows(); ++i)
+            for (long j = 0; j < ro.tiles[t].cols(); ++j) same_on &= ro.tiles[t](i, j) == rr.tiles[t](i, j);
+    CHECK(same_on);
+    CHECK(ro.timing.mode == "online");
     // missing frames are reported (test_recon.cpp:183-190)
     FrameSet one = fs;
     one.frames.resize(1);

@@ -131,12 +131,14 @@ def test_epry_defocused_tile_final(orc, eng):
     assert amp < FINAL_TOL and ph < FINAL_TOL, (amp, ph)
 
 
-def test_pipelined_bit_identical_to_sequential(eng):
-    """Spectrum-domain level: pipelined == sequential bit for bit (test_parallel.cpp:79-122)."""
-    cfg = gpu_cfg(led_scan_rows=7, led_scan_cols=7, tile_overlap=0)
+@pytest.mark.parametrize("n", [64, 128, 256])
+def test_pipelined_bit_identical_to_sequential(eng, n):
+    """Spectrum-domain level: pipelined == sequential bit for bit (test_parallel.cpp:79-122),
+    on the lattice kernel (n = 64) and the general warp-FFT kernel (n = 128, 256)."""
+    cfg = gpu_cfg(tile_size=n, led_scan_rows=7, led_scan_cols=7, tile_overlap=0)
     fs, _, _, _ = dataset(cfg, seed=23)
     seq = fpm.led_sequence("raster", cfg)
-    t = fpm.partition_tiles(64, 64, cfg)[0]
+    t = fpm.partition_tiles(n, n, cfg)[0]
     lag = fpm.min_safe_lag_tile(seq, t, cfg)
     assert lag < len(seq)
     a = fpm.reconstruct_tile(fs, t, cfg, 3, seq, engine=eng)
