@@ -159,6 +159,24 @@ bool box_forced() {
     return e && e[0] == '1';
 }
 
+// Cluster split of a tile (kernels_cluster.cu): n = 256, whose box-row
+// intermediate (240 KB) needs two SMs' shared memory, and n = 128 batches too
+// small to occupy the GPU with one CTA per tile. FPM_B200_CLUSTER=<cl> forces a
+// size (1 = off).
+int cluster_choice(int n, int N, int T) {
+    if (const char* e = std::getenv("FPM_B200_CLUSTER")) {
+        const int c = std::atoi(e);
+        if (c <= 1) return 0;
+        if (!fpmk::cluster_supported(n, N, c))
+            throw Unsupported("no cluster kernel for n = " + std::to_string(n) + ", N = " + std::to_string(N) +
+                              ", cluster " + std::to_string(c));
+        return c;
+    }
+    if (n == 256 && N == 1024) return 2;
+    if (n == 128 && N == 512 && T * 8 <= 148) return 8;
+    return 0;
+}
+
 std::vector<float2> twiddles(int N) {
     std::vector<float2> w(static_cast<size_t>(N));
     for (int m = 0; m < N; ++m) {
@@ -205,6 +223,7 @@ struct fpmgpu_plan {
     int n = 0, N = 0, T = 0, L = 0, F = 0, G = 1, lag = 0, nslots = 1, num_slots = 0;
     bool prune = false;
     bool use_box = false;  // n != 64: warp-FFT box kernel (kernels_box.cu)
+    int cl = 0;            // > 0: each tile split over a cluster of cl CTAs (kernels_cluster.cu)
     int box = 0, b0 = 0;
     int support_px = 0;
     double radius = 0.0;
@@ -280,7 +299,12 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     p.bright.upload(bright.data(), bright.size(), p.ctx->stream);
     p.support_px = 0;
     for (auto s : sup) p.support_px += s;
-    if (p.use_box) {
+    p.cl = box_forced() ? 0 : cluster_choice(p.n, p.N, p.T);
+    if (p.cl) {
+        box_of(sup, p.n, &p.b0, &p.box);
+        if (fpmk::cluster_smem_bytes(p.n, p.box, p.cl, fpmk::cluster_warps(p.n, p.cl), p.L, r.iters) > 232448)
+            throw Unsupported("cluster slab exceeds shared memory");
+    } else if (p.use_box) {
         box_of(sup, p.n, &p.b0, &p.box);
         const bool smem_s = p.n != 256;
         if (p.n == 256 && p.N != 1024) throw Unsupported("n = 256 runs with canvas side 1024 (upsample 4) in this build");
@@ -402,7 +426,7 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
     a.nslots = p.nslots;
     a.alpha = float(r.alpha);
     a.beta = float(r.beta);
-    if (p.use_box) {
+    if (p.use_box || p.cl) {
         fpmk::BoxArgs bx{};
         bx.scratch = p.scratch.p;
         bx.frames = frames;
@@ -410,7 +434,10 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
         bx.frame_stride = pitch * r.height;
         bx.box = p.box;
         bx.b0 = p.b0;
-        ck(fpmk::launch_loop_box(p.n, r.mode, a, bx, p.T, s), "LED loop (box)");
+        if (p.cl)
+            ck(fpmk::launch_loop_cluster(p.n, r.mode, p.cl, a, bx, p.T, s), "LED loop (cluster)");
+        else
+            ck(fpmk::launch_loop_box(p.n, r.mode, a, bx, p.T, s), "LED loop (box)");
     } else {
         const CUtensorMap map = encode_frames_map(frames, p.F, r.height, r.width, pitch);
         ck(fpmk::launch_loop64(r.mode, p.prune, fpmk::kMeasTMA, p.G, &map, a, p.T, s), "LED loop");
@@ -821,10 +848,13 @@ int fpmgpu_plan_get_info(const fpmgpu_plan* p, fpmgpu_plan_info* info) {
         info->lag = p->lag;
         info->groups = p->G;
         info->launches_per_execute = (p->has_pupils ? 0 : 1) + 2 + 1 + 2;
-        info->loop_ctas = p->T;
-        info->loop_threads = p->use_box ? 512 : 128 * p->G;
-        info->loop_smem_bytes = int(p->use_box ? fpmk::box_smem_bytes(p->n, p->box, p->L, p->req.iters, p->n != 256)
-                                               : fpmk::loop_smem_bytes(p->G, p->nslots, p->L, p->req.iters));
+        info->loop_ctas = p->T * (p->cl ? p->cl : 1);
+        info->loop_threads = p->cl ? 32 * fpmk::cluster_warps(p->n, p->cl) : p->use_box ? 512 : 128 * p->G;
+        info->loop_smem_bytes =
+            int(p->cl ? fpmk::cluster_smem_bytes(p->n, p->box, p->cl, fpmk::cluster_warps(p->n, p->cl), p->L,
+                                                 p->req.iters)
+                : p->use_box ? fpmk::box_smem_bytes(p->n, p->box, p->L, p->req.iters, p->n != 256)
+                             : fpmk::loop_smem_bytes(p->G, p->nslots, p->L, p->req.iters));
         info->updates = double(p->T) * p->L * p->req.iters;
         info->fft_flops_per_update = 20.0 * p->n * p->n * std::log2(double(p->n));
         info->hbm_bytes_per_update = 2.0 * p->n * p->n + 16.0 * p->support_px;

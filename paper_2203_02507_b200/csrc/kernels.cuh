@@ -54,6 +54,13 @@ struct BoxArgs {
 size_t box_smem_bytes(int n, int box, int L, int iters, bool scratch_in_smem);
 cudaError_t launch_loop_box(int n, int mode, const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s);
 
+// One tile split over a cluster of cl CTAs (kernels_cluster.cu).
+size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters);
+int cluster_warps(int n, int cl);
+bool cluster_supported(int n, int N, int cl);
+cudaError_t launch_loop_cluster(int n, int mode, int cl, const LoopArgs& a, const BoxArgs& b, int T,
+                                cudaStream_t s);
+
 size_t loop_smem_bytes(int G, int nslots, int L, int iters);
 
 #ifdef __CUDACC__

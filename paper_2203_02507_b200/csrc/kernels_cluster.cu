@@ -1,0 +1,313 @@
+// fpm_loop_cluster: the fused per-LED update with one tile split over a
+// thread-block cluster of CL CTAs (distributed shared memory), persistent over
+// the LED loop. Same arithmetic as fpm_loop_box (kernels_box.cu), so the two
+// produce the same canvas bit for bit; what changes is where the work runs:
+//
+//   A  rows i = b0 + rank + CL t of the pupil box: gather the disk x P', IFFT
+//      (warp F2), and scatter each row's n outputs to the CTA owning those
+//      columns — column slab c holds columns [c n/CL, (c+1) n/CL) of all B box
+//      rows (DSMEM stores, 32 consecutive elements per lane group)
+//   -- cluster barrier --
+//   B  the CTA's own columns: IFFT over the box rows (F1) -> modulus with
+//      sqrt(I) -> FFT (F2) -> keep the box rows; the measurement slab is staged
+//      column-major with rows permuted (k0, t) so the modulus reads are
+//      conflict-free
+//   -- cluster barrier -- (residual and EPRY maxima reduced over the cluster)
+//   C  the same rows as A: fetch the row from the column slabs (DSMEM loads),
+//      FFT (F1), scatter into the canvas disk (GS / EPRY)
+//   -- cluster barrier -- (slabs free; canvas writes visible cluster-wide)
+//
+// A row's canvas disk moves with the LED, so consecutive updates read canvas
+// rows another CTA of the cluster wrote: the third barrier (release/acquire at
+// cluster scope) orders them. Use: n = 256 tiles, whose B x n intermediate
+// (240 KB) does not fit one SM, and single-tile runs, where one CTA would
+// leave 147 SMs idle (BASELINE configs 1-2).
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+#include "warp_fft.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fpmk {
+
+size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
+    const size_t sw = size_t(n / cl);
+    size_t b = size_t(box) * (sw + 1) * sizeof(float2);  // column slab of the box rows
+    b += sw * (size_t(n) + 2) * sizeof(uint16_t);         // measurement slab
+    b = (b + 15) & ~size_t(15);
+    b += size_t(iters) * sizeof(double);
+    b += size_t(nw) * 4 * sizeof(float) + 4 * sizeof(float);
+    b += size_t(L) * (sizeof(short2) + sizeof(int) + 1) + 16;
+    return b;
+}
+
+namespace {
+
+template <int NLR, int MODE, int NC, int CL, int NW>
+__global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args, const BoxArgs bx) {
+    constexpr int M = NLR / 32;
+    constexpr int SW = NLR / CL;  // columns per CTA
+    constexpr int RS = SW + 1;    // slab row stride (float2): column reads conflict-free
+    constexpr int IS = NLR + 2;   // measurement slab column stride (u16): staging stores conflict-free
+    constexpr int NT = NW * 32;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = int(cluster.block_rank());
+    const int tile = blockIdx.x / CL;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int L = args.L, B = bx.box, b0 = bx.b0;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* sp = smem_raw;
+    float2* S = reinterpret_cast<float2*>(sp);
+    sp += size_t(B) * RS * sizeof(float2);
+    uint16_t* I_s = reinterpret_cast<uint16_t*>(sp);
+    sp += size_t(SW) * IS * sizeof(uint16_t);
+    sp = smem_raw + ((sp - smem_raw + 15) & ~15);
+    double* stage_sum = reinterpret_cast<double*>(sp);
+    sp += size_t(args.iters) * sizeof(double);
+    float* wred = reinterpret_cast<float*>(sp);  // [warp][4]: num, den, omax, pmax
+    sp += NW * 4 * sizeof(float);
+    float* upd = reinterpret_cast<float*>(sp);  // inv_omax, inv_pmax of the current update
+    sp += 4 * sizeof(float);
+    short2* O_s = reinterpret_cast<short2*>(sp);
+    sp += size_t(L) * sizeof(short2);
+    int* F_s = reinterpret_cast<int*>(sp);
+    sp += size_t(L) * sizeof(int);
+    uint8_t* B_s = sp;
+
+    float2* canvas = args.canvas + size_t(tile) * NC * NC;
+    float2* pupil = args.pupils + size_t(tile) * NLR * NLR;
+    const uint8_t* sup = args.support;
+    const int2 txy = args.tile_xy[tile];
+    for (int k = threadIdx.x; k < L; k += NT) {
+        O_s[k] = args.origins[size_t(tile) * L + k];
+        F_s[k] = args.seq_frame[k];
+        B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
+    }
+    for (int k = threadIdx.x; k < args.iters; k += NT) stage_sum[k] = 0.0;
+    WarpFFT<M> F;
+    F.init(l, NLR);
+    const float inv_n2 = 1.0f / float(NLR * NLR);
+    cluster.sync();  // every CTA of the cluster is resident before any DSMEM access
+
+    const int G = args.slots ? 2 : 1;
+    for (int e = args.slot_begin * G; e < args.num_slots * G; ++e) {
+        int it, pos;
+        if (G == 1) {
+            it = e / L;
+            pos = e % L;
+        } else {
+            const int2 en = args.slots[e];
+            if (en.x < 0) continue;
+            it = en.x;
+            pos = en.y;
+        }
+        const short2 o = O_s[pos];
+        float2* cv = canvas + size_t(o.x) * NC + o.y;
+
+        // ---- measurement slab: rows r, columns rank SW + jj, stored at [jj][(r mod M) n/M + r / M]
+        {
+            const uint16_t* fr =
+                bx.frames + size_t(F_s[pos]) * bx.frame_stride + size_t(txy.y) * bx.pitch + txy.x + rank * SW;
+            for (int idx = threadIdx.x; idx < NLR * SW; idx += NT) {
+                const int r = idx / SW, jj = idx % SW;
+                I_s[jj * IS + (r % M) * (NLR / M) + r / M] = fr[size_t(r) * bx.pitch + jj];
+            }
+        }
+
+        // ---- A: IFFT of this CTA's box rows, outputs to the column owners
+        float omax = 0.f, pmax = 0.f;
+        for (int i = b0 + rank + CL * w; i < b0 + B; i += CL * NW) {
+            float2 x[M];
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const int c = k0 + M * brev5(l);
+                float2 v = make_float2(0.f, 0.f);
+                if (sup[i * NLR + c]) {
+                    const float2 O = cv[size_t(i) * NC + c];
+                    const float2 P = pupil[i * NLR + c];
+                    v = cscale(cmul(O, P), ((i + c) & 1) ? -1.f : 1.f);
+                    if (MODE == kModeEPRY) {
+                        omax = fmaxf(omax, cabs2(O));
+                        pmax = fmaxf(pmax, cabs2(P));
+                    }
+                }
+                x[k0] = v;
+            }
+            F.template f2<true>(x);
+#pragma unroll
+            for (int r = 0; r < M; ++r) {
+                const int col = l + 32 * r, owner = col / SW;
+                cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)] = x[r];
+            }
+        }
+        if (MODE == kModeEPRY) {
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                omax = fmaxf(omax, __shfl_xor_sync(kFull, omax, sh));
+                pmax = fmaxf(pmax, __shfl_xor_sync(kFull, pmax, sh));
+            }
+            if (l == 0) {
+                wred[w * 4 + 2] = omax;
+                wred[w * 4 + 3] = pmax;
+            }
+        }
+        cluster.sync();
+
+        // ---- B: this CTA's columns: IFFT over the box rows -> modulus -> FFT -> box rows
+        float num = 0.f, den = 0.f;
+        for (int jj = w; jj < SW; jj += NW) {
+            const int j = rank * SW + jj;
+            float2 x[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const int r = l + 32 * m;
+                x[m] = (r >= b0 && r < b0 + B) ? S[size_t(r - b0) * RS + jj] : make_float2(0.f, 0.f);
+            }
+            F.template f1<true>(x);
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const int row = k0 + M * brev5(l);
+                const float Iv = float(I_s[jj * IS + k0 * (NLR / M) + brev5(l)]);
+                den += Iv;
+                // branch-free: |e|^2 at or below FLT_MIN counts as |e| = 0 (recon.cpp:122)
+                const float meas = sqrt_ftz(Iv);
+                const float2 u = x[k0];
+                const float m2 = cabs2(u);
+                const bool nz = m2 > kTiny;
+                const float rr = rsqrt_ftz(fmaxf(m2, kTiny));
+                const float dm = fmaf(m2 * rr, inv_n2, -meas);
+                num = fmaf(dm, dm, num);
+                const float sc = nz ? meas * rr : 0.f;
+                const float z = nz ? 0.f : (((row + j) & 1) ? -meas : meas);
+                x[k0] = make_float2(fmaf(u.x, sc, z), u.y * sc);
+            }
+            F.template f2<false>(x);
+#pragma unroll
+            for (int r = 0; r < M; ++r) {
+                const int row = l + 32 * r;
+                if (row >= b0 && row < b0 + B) S[size_t(row - b0) * RS + jj] = x[r];
+            }
+        }
+#pragma unroll
+        for (int sh = 16; sh; sh >>= 1) {
+            num += __shfl_xor_sync(kFull, num, sh);
+            den += __shfl_xor_sync(kFull, den, sh);
+        }
+        if (l == 0) {
+            wred[w * 4] = num;
+            wred[w * 4 + 1] = den;
+        }
+        cluster.sync();
+
+        // ---- cluster-wide residual terms and EPRY maxima (fixed order: deterministic)
+        if (w == 0) {
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            for (int k = l; k < CL * NW; k += 32) {
+                const float* src = cluster.map_shared_rank(wred, k / NW) + (k % NW) * 4;
+                a0 += src[0];
+                a1 += src[1];
+                if (MODE == kModeEPRY) {
+                    a2 = fmaxf(a2, src[2]);
+                    a3 = fmaxf(a3, src[3]);
+                }
+            }
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) {
+                a0 += __shfl_xor_sync(kFull, a0, sh);
+                a1 += __shfl_xor_sync(kFull, a1, sh);
+                a2 = fmaxf(a2, __shfl_xor_sync(kFull, a2, sh));
+                a3 = fmaxf(a3, __shfl_xor_sync(kFull, a3, sh));
+            }
+            if (l == 0) {
+                if (rank == 0) stage_sum[it] += a1 > 0.f ? double(a0) / double(a1) : 0.0;
+                upd[0] = (a2 > 0.f && B_s[pos]) ? args.beta / a2 : 0.f;  // bright-field pupil steps only
+                upd[1] = a3 > 0.f ? args.alpha / a3 : 0.f;
+            }
+        }
+        __syncthreads();
+        const float inv_omax = upd[0], inv_pmax = upd[1];
+
+        // ---- C: FFT of this CTA's box rows (fetched from the column slabs), scatter
+        for (int i = b0 + rank + CL * w; i < b0 + B; i += CL * NW) {
+            float2 x[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const int col = l + 32 * m, owner = col / SW;
+                x[m] = cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)];
+            }
+            F.template f1<false>(x);
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const int c = k0 + M * brev5(l);
+                if (!sup[i * NLR + c]) continue;
+                const float2 psi2 = cscale(x[k0], ((i + c) & 1) ? -1.f : 1.f);
+                float2* dst = cv + size_t(i) * NC + c;
+                float2* pp = pupil + i * NLR + c;
+                const float2 P = *pp;
+                if (MODE == kModeGS) {
+                    *dst = cmulc(psi2, P);
+                } else {
+                    const float2 O = *dst;
+                    const float2 d = csub(psi2, cmul(O, P));
+                    if (inv_pmax > 0.f) *dst = cadd(O, cscale(cmulc(d, P), inv_pmax));
+                    if (inv_omax > 0.f) *pp = cadd(P, cscale(cmulc(d, O), inv_omax));
+                }
+            }
+        }
+        cluster.sync();  // slabs reusable; canvas and pupil writes visible to the whole cluster
+    }
+    if (rank == 0) store_residuals(args, tile, stage_sum, G == 1);
+}
+
+template <int NLR, int MODE, int NC, int CL, int NW>
+cudaError_t launch_cluster_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s) {
+    const size_t smem = cluster_smem_bytes(NLR, b.box, CL, NW, a.L, a.iters);
+    auto k = fpm_loop_cluster<NLR, MODE, NC, CL, NW>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(T * CL));
+    cfg.blockDim = dim3(NW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, a, b);
+}
+
+}  // namespace
+
+int cluster_warps(int n, int cl) { return n == 64 ? 4 : (n == 256 && cl == 2) ? 16 : 8; }
+
+bool cluster_supported(int n, int N, int cl) {
+    if (n == 64) return N == 256 && (cl == 4 || cl == 8);
+    if (n == 128) return N == 512 && (cl == 2 || cl == 4 || cl == 8);
+    if (n == 256) return N == 1024 && (cl == 2 || cl == 4 || cl == 8);
+    return false;
+}
+
+cudaError_t launch_loop_cluster(int n, int mode, int cl, const LoopArgs& a, const BoxArgs& b, int T,
+                                cudaStream_t s) {
+#define FPM_CL_CASE(NN, NCC, CLL, NWW)                                                          \
+    if (n == NN && a.N == NCC && cl == CLL)                                                     \
+        return mode == kModeGS ? launch_cluster_t<NN, kModeGS, NCC, CLL, NWW>(a, b, T, s)       \
+                               : launch_cluster_t<NN, kModeEPRY, NCC, CLL, NWW>(a, b, T, s);
+    FPM_CL_CASE(64, 256, 4, 4)
+    FPM_CL_CASE(64, 256, 8, 4)
+    FPM_CL_CASE(128, 512, 2, 8)
+    FPM_CL_CASE(128, 512, 4, 8)
+    FPM_CL_CASE(128, 512, 8, 8)
+    FPM_CL_CASE(256, 1024, 2, 16)
+    FPM_CL_CASE(256, 1024, 4, 8)
+    FPM_CL_CASE(256, 1024, 8, 8)
+#undef FPM_CL_CASE
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace fpmk

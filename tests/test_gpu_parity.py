@@ -306,3 +306,36 @@ def test_banded_host_path_bit_identical(eng, monkeypatch, bands):
     assert a.pupils is not None
     for pa, pb in zip(a.pupils, b.pupils):
         assert np.array_equal(pa, pb)
+
+
+@pytest.mark.parametrize("n,cl,mode", [(128, 2, "epry"), (128, 4, "gs"), (128, 8, "epry"), (256, 2, "gs"),
+                                       (256, 4, "epry"), (256, 8, "gs")])
+def test_cluster_kernel_matches_box_kernel(eng, monkeypatch, n, cl, mode):
+    """A tile split over a CTA cluster (DSMEM column slabs) runs the box kernel's
+    arithmetic element for element: same canvas bits, same pupil bits."""
+    cfg = fpm.OpticalConfig(tile_size=n, tile_overlap=0, upsample=4, led_scan_rows=5, led_scan_cols=5)
+    fs, _, seq, _ = dataset(cfg, seed=40, defocus_um=6.0)
+    t = fpm.partition_tiles(n, n, cfg)[0]
+    t.defocus_um = 4.0
+    monkeypatch.setenv("FPM_B200_CLUSTER", "1")
+    a = fpm.reconstruct_tile(fs, t, cfg, 2, seq, mode=mode, engine=fpm.Engine(0))
+    monkeypatch.setenv("FPM_B200_CLUSTER", str(cl))
+    b = fpm.reconstruct_tile(fs, t, cfg, 2, seq, mode=mode, engine=fpm.Engine(0))
+    assert np.array_equal(a.hr, b.hr)
+    if mode == "epry":
+        assert np.array_equal(a.pupil, b.pupil)
+    assert np.allclose(a.metrics.pass_mean_residual, b.metrics.pass_mean_residual, rtol=1e-5)
+
+
+@pytest.mark.parametrize("cl", [4, 8])
+def test_cluster_kernel_n64_matches_oracle(orc, eng, monkeypatch, cl):
+    """n = 64 on the cluster kernel (single-tile latency path) against the oracle."""
+    cfg = gpu_cfg(led_scan_rows=7, led_scan_cols=7)
+    fs, ofs, seq, _ = dataset(cfg, seed=41)
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    monkeypatch.setenv("FPM_B200_CLUSTER", str(cl))
+    got = fpm.reconstruct_tile(fs, t, cfg, 2, seq, mode="epry", engine=fpm.Engine(0))
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), 2, seq, mode="epry")
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
+    assert np.allclose(got.metrics.pass_mean_residual, ref.residuals, rtol=1e-3)
