@@ -137,6 +137,26 @@ __device__ __forceinline__ void dft8x8(float2 (&v)[8][8]) {
         dft8<INV, PRUNE>(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4], v[a][5], v[a][6], v[a][7]);
 }
 
+// radix-4 butterfly with a0 = a3 = 0 on entry (the pruned IFFT's zero columns):
+// s02 = a2, d02 = -a2, s13 = a1, d13 = w a1 -> four FADD2 instead of eight
+template <bool INV>
+__device__ __forceinline__ void dft4_z03(float2& a0, float2& a1, float2& a2, float2& a3) {
+    const float2 x1 = a1, x2 = a2, d13 = w8_2<INV>(x1);
+    a0 = cadd(x2, x1);
+    a2 = csub(x2, x1);
+    a1 = csub(d13, x2);
+    a3 = csub(cneg(x2), d13);
+}
+
+// radix-4 butterfly producing only outputs 1 and 2 (the pruned FFT's scatter columns)
+template <bool INV>
+__device__ __forceinline__ void dft4_o12(float2& a0, float2& a1, float2& a2, float2& a3) {
+    const float2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
+    const float2 s13 = cadd(a1, a3), d13 = w8_2<INV>(csub(a1, a3));
+    a1 = cadd(d02, d13);
+    a2 = csub(s02, s13);
+}
+
 // radix-4 butterfly on natural-order inputs (fwd: W4 = -i)
 template <bool INV>
 __device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {

@@ -100,15 +100,24 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
                                                 float sg, const float2 (&tw)[4], const float2 (&twsw)[4], int g,
                                                 bool skip_cols, bool skip_rows) {
     const int tr = p >> 3, tc = p & 7;
-    // step 1: DFT8 over n1r (registers), then the pair DFT over n1c (DIT)
+    // step 1: DFT8 over n1r (registers), then the pair DFT over n1c (DIT). Pruned IFFT
+    // (skip_cols): only rows a in [2, 6) of columns j in {1, 2} hold data, and the
+    // zero entries are never read (they need no initialisation)
+    if (skip_cols) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if ((j == 0 || j == 3) && skip_cols) continue;
-        dft8<false, false>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
+        for (int j = 1; j < 3; ++j)
+            dft8<false, true>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) dft4_z03<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            dft8<false, false>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);  // E (h = 0) or O (h = 1)
     }
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
-        dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);  // E (h = 0) or O (h = 1)
 #pragma unroll
         for (int m = 1; m < 4; ++m) v[a][m] = cmul_sw(v[a][m], tw[m], twsw[m]);  // O' = W8^m O
 #pragma unroll
@@ -162,7 +171,10 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
         for (int i = 0; i < 4; ++i) v[a][i] = cfma(sg, v[a][i], shfl_pair(v[a][i]));  // y_i + y_(i+4) | y_i - y_(i+4)
 #pragma unroll
         for (int i = 1; i < 4; ++i) v[a][i] = cmul_sw(v[a][i], tw[i], twsw[i]);
-        dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
+        if (skip_rows)  // the scatter reads columns j in {1, 2} of these rows only
+            dft4_o12<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
+        else
+            dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
     }
 }
 
@@ -303,11 +315,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
 
             // ---- gather: every disk load in flight at once (all lattice addresses lie in
             // the n x n block, so the loads need no predicate), then times P'
-            float2 v[8][4];
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) v[a][j] = make_float2(0.f, 0.f);
+            float2 v[8][4];  // lattice positions outside the disk block are never read (pruned IFFT)
 #pragma unroll
             for (int q = 0; q < NP; ++q) v[Lat::a(q)][Lat::j(q)] = cv[Lat::a(q) * 8 * N + 16 * Lat::j(q)];
             // EPRY maxima (block-uniform branches): max|O_D|^2 only for bright-field updates (the
