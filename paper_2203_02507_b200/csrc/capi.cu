@@ -172,7 +172,7 @@ int cluster_choice(int n, int N, int T) {
                               ", cluster " + std::to_string(c));
         return c;
     }
-    if (n == 256 && N == 1024) return 2;
+    if (n == 256 && N == 1024) return 4;
     if (n == 128 && N == 512 && T * 8 <= 148) return 8;
     return 0;
 }
@@ -229,6 +229,7 @@ struct fpmgpu_plan {
     double radius = 0.0;
     DevBuf<float2> canvas, pupils, pupils_init, scratch;
     DevBuf<uint8_t> support;
+    DevBuf<short2> sup_rows;
     DevBuf<short2> origins;
     DevBuf<uint8_t> bright;
     DevBuf<int> seq_frame;
@@ -302,6 +303,19 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     p.cl = box_forced() ? 0 : cluster_choice(p.n, p.N, p.T);
     if (p.cl) {
         box_of(sup, p.n, &p.b0, &p.box);
+        std::vector<short2> runs(size_t(p.n), make_short2(0, 0));
+        for (int i = 0; i < p.n; ++i) {
+            int lo = p.n, hi = 0;
+            for (int j = 0; j < p.n; ++j)
+                if (sup[size_t(i) * p.n + j]) {
+                    lo = std::min(lo, j);
+                    hi = j + 1;
+                }
+            for (int j = lo; j < hi; ++j)
+                if (!sup[size_t(i) * p.n + j]) throw ConfigError("pupil support row is not one run");
+            if (hi > lo) runs[size_t(i)] = make_short2(short(lo), short(hi));
+        }
+        p.sup_rows.upload(runs.data(), runs.size(), p.ctx->stream);
         if (fpmk::cluster_smem_bytes(p.n, p.box, p.cl, fpmk::cluster_warps(p.n, p.cl), p.L, r.iters) > 232448)
             throw Unsupported("cluster slab exceeds shared memory");
     } else if (p.use_box) {
@@ -434,6 +448,7 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
         bx.frame_stride = pitch * r.height;
         bx.box = p.box;
         bx.b0 = p.b0;
+        bx.sup_rows = p.sup_rows.p;
         if (p.cl)
             ck(fpmk::launch_loop_cluster(p.n, r.mode, p.cl, a, bx, p.T, s), "LED loop (cluster)");
         else

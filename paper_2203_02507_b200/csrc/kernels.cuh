@@ -50,6 +50,7 @@ struct BoxArgs {
     long long pitch;            // elements
     long long frame_stride;     // elements per frame
     int box, b0;                // pupil bounding box: rows/cols [b0, b0 + box)
+    const short2* sup_rows;     // [n] support columns [x, y) of each row (a disk: one run per row)
 };
 size_t box_smem_bytes(int n, int box, int L, int iters, bool scratch_in_smem);
 cudaError_t launch_loop_box(int n, int mode, const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s);

@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
                 if (sup[i * NLR + c]) {
                     const float2 O = cvc[size_t(i) * NC + c];
                     const float2 P = pupil[i * NLR + c];
-                    v = cscale(cmul(O, P), ((i + c) & 1) ? -1.f : 1.f);
+                    const float2 g = cmul(O, P);  // conj, signed: the row IFFT runs as conj(FFT(conj g))
+                    v = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
                     if (MODE == kModeEPRY) {
                         omax = fmaxf(omax, cabs2(O));
                         pmax = fmaxf(pmax, cabs2(P));
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
                 }
                 x[k0] = v;
             }
-            F.template f2<true>(x);
+            F.f2(x);  // S keeps conj(IFFT_rows(g)): phase B's forward column FFT undoes it
 #pragma unroll
             for (int r = 0; r < M; ++r) S[size_t(i - b0) * RS + l + 32 * r] = x[r];
         }
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
                 const int r = l + 32 * m;
                 x[m] = (r >= b0 && r < b0 + B) ? S[size_t(r - b0) * RS + j] : make_float2(0.f, 0.f);
             }
-            F.template f1<true>(x);
+            F.f1(x);  // = conj(e), e the unscaled 2-D IFFT
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int row = k0 + M * brev5(l);
@@ -177,9 +178,9 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
                 num = fmaf(dm, dm, num);
                 const float sc = nz ? meas * rr : 0.f;
                 const float z = nz ? 0.f : (((row + j) & 1) ? -meas : meas);
-                x[k0] = make_float2(fmaf(u.x, sc, z), u.y * sc);
+                x[k0] = make_float2(fmaf(u.x, sc, z), -u.y * sc);  // e' from u = conj(e)
             }
-            F.template f2<false>(x);
+            F.f2(x);
 #pragma unroll
             for (int r = 0; r < M; ++r) {
                 const int row = l + 32 * r;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
             float2 x[M];
 #pragma unroll
             for (int m = 0; m < M; ++m) x[m] = S[size_t(i - b0) * RS + l + 32 * m];
-            F.template f1<false>(x);
+            F.f1(x);
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int c = k0 + M * brev5(l);

@@ -34,7 +34,8 @@ namespace fpmk {
 size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
     const size_t sw = size_t(n / cl);
     size_t b = size_t(box) * (sw + 1) * sizeof(float2);  // column slab of the box rows
-    b += sw * (size_t(n) + 2) * sizeof(uint16_t);         // measurement slab
+    b += sw * size_t(n) * sizeof(uint16_t);               // measurement slab
+    b += size_t(n) * sizeof(short2);                      // support run per row
     b = (b + 15) & ~size_t(15);
     b += size_t(iters) * sizeof(double);
     b += size_t(nw) * 4 * sizeof(float) + 4 * sizeof(float);
@@ -44,12 +45,20 @@ size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
 
 namespace {
 
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int NLR, int MODE, int NC, int CL, int NW>
 __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args, const BoxArgs bx) {
     constexpr int M = NLR / 32;
     constexpr int SW = NLR / CL;  // columns per CTA
     constexpr int RS = SW + 1;    // slab row stride (float2): column reads conflict-free
-    constexpr int IS = NLR + 2;   // measurement slab column stride (u16): staging stores conflict-free
     constexpr int NT = NW * 32;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = int(cluster.block_rank());
@@ -60,8 +69,10 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
     uint8_t* sp = smem_raw;
     float2* S = reinterpret_cast<float2*>(sp);
     sp += size_t(B) * RS * sizeof(float2);
-    uint16_t* I_s = reinterpret_cast<uint16_t*>(sp);
-    sp += size_t(SW) * IS * sizeof(uint16_t);
+    uint16_t* I_s = reinterpret_cast<uint16_t*>(sp);  // [row][column ^ isw(row)]
+    sp += size_t(SW) * NLR * sizeof(uint16_t);
+    short2* SR = reinterpret_cast<short2*>(sp);  // support run [x, y) of each row
+    sp += size_t(NLR) * sizeof(short2);
     sp = smem_raw + ((sp - smem_raw + 15) & ~15);
     double* stage_sum = reinterpret_cast<double*>(sp);
     sp += size_t(args.iters) * sizeof(double);
@@ -77,8 +88,8 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
 
     float2* canvas = args.canvas + size_t(tile) * NC * NC;
     float2* pupil = args.pupils + size_t(tile) * NLR * NLR;
-    const uint8_t* sup = args.support;
     const int2 txy = args.tile_xy[tile];
+    for (int k = threadIdx.x; k < NLR; k += NT) SR[k] = bx.sup_rows[k];
     for (int k = threadIdx.x; k < L; k += NT) {
         O_s[k] = args.origins[size_t(tile) * L + k];
         F_s[k] = args.seq_frame[k];
@@ -90,43 +101,74 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
     const float inv_n2 = 1.0f / float(NLR * NLR);
     cluster.sync();  // every CTA of the cluster is resident before any DSMEM access
 
+    // schedule entries: sequential slot e = (e / L, e % L); pipelined slots hold two
+    // entries each (stage < 0 = idle), run back to back
     const int G = args.slots ? 2 : 1;
-    for (int e = args.slot_begin * G; e < args.num_slots * G; ++e) {
-        int it, pos;
+    const int e_end = args.num_slots * G;
+    auto entry_at = [&](int e, int& it, int& pos) -> bool {
         if (G == 1) {
             it = e / L;
             pos = e % L;
-        } else {
-            const int2 en = args.slots[e];
-            if (en.x < 0) continue;
-            it = en.x;
-            pos = en.y;
+            return true;
         }
-        const short2 o = O_s[pos];
-        float2* cv = canvas + size_t(o.x) * NC + o.y;
-
-        // ---- measurement slab: rows r, columns rank SW + jj, stored at [jj][(r mod M) n/M + r / M]
-        {
-            const uint16_t* fr =
-                bx.frames + size_t(F_s[pos]) * bx.frame_stride + size_t(txy.y) * bx.pitch + txy.x + rank * SW;
+        const int2 en = args.slots[e];
+        it = en.x;
+        pos = en.y;
+        return en.x >= 0;
+    };
+    auto next_entry = [&](int e) -> int {
+        int a, b;
+        for (int f = e + 1; f < e_end; ++f)
+            if (entry_at(f, a, b)) return f;
+        return -1;
+    };
+    // measurement slab of one update: rows r, columns rank SW + jj at [r][jj ^ isw(r)]
+    // (XOR on pairs: the modulus reads of rows k0 + M t land in distinct banks); staged
+    // asynchronously one update ahead by 4-byte cp.async, consumed only by phase B
+    const bool even_x = ((txy.x + rank * SW) & 1) == 0;
+    auto stage = [&](int pos) {
+        const uint16_t* fr =
+            bx.frames + size_t(F_s[pos]) * bx.frame_stride + size_t(txy.y) * bx.pitch + txy.x + rank * SW;
+        if (even_x) {
+            for (int idx = threadIdx.x; idx < NLR * SW / 2; idx += NT) {
+                const int r = idx / (SW / 2), jp = 2 * (idx % (SW / 2));
+                cp_async4(I_s + r * SW + (jp ^ ((2 * (r / M)) & (SW - 1))), fr + size_t(r) * bx.pitch + jp);
+            }
+            cp_async_commit();
+        } else {
             for (int idx = threadIdx.x; idx < NLR * SW; idx += NT) {
                 const int r = idx / SW, jj = idx % SW;
-                I_s[jj * IS + (r % M) * (NLR / M) + r / M] = fr[size_t(r) * bx.pitch + jj];
+                I_s[r * SW + (jj ^ ((2 * (r / M)) & (SW - 1)))] = fr[size_t(r) * bx.pitch + jj];
             }
         }
+    };
+    int e = next_entry(args.slot_begin * G - 1);
+    if (e >= 0) {
+        int it0, pos0;
+        entry_at(e, it0, pos0);
+        stage(pos0);
+    }
+    for (; e >= 0;) {
+        int it, pos;
+        entry_at(e, it, pos);
+        const int e_next = next_entry(e);
+        const short2 o = O_s[pos];
+        float2* cv = canvas + size_t(o.x) * NC + o.y;
 
         // ---- A: IFFT of this CTA's box rows, outputs to the column owners
         float omax = 0.f, pmax = 0.f;
         for (int i = b0 + rank + CL * w; i < b0 + B; i += CL * NW) {
             float2 x[M];
+            const short2 run = SR[i];
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int c = k0 + M * brev5(l);
                 float2 v = make_float2(0.f, 0.f);
-                if (sup[i * NLR + c]) {
+                if (c >= run.x && c < run.y) {
                     const float2 O = cv[size_t(i) * NC + c];
                     const float2 P = pupil[i * NLR + c];
-                    v = cscale(cmul(O, P), ((i + c) & 1) ? -1.f : 1.f);
+                    const float2 g = cmul(O, P);  // conj, signed: the row IFFT runs as conj(FFT(conj g))
+                    v = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
                     if (MODE == kModeEPRY) {
                         omax = fmaxf(omax, cabs2(O));
                         pmax = fmaxf(pmax, cabs2(P));
@@ -134,7 +176,7 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
                 }
                 x[k0] = v;
             }
-            F.template f2<true>(x);
+            F.f2(x);  // S keeps conj(IFFT_rows(g)): phase B's forward column FFT undoes it
 #pragma unroll
             for (int r = 0; r < M; ++r) {
                 const int col = l + 32 * r, owner = col / SW;
@@ -152,6 +194,7 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
                 wred[w * 4 + 3] = pmax;
             }
         }
+        cp_async_wait_all();  // this thread's part of the measurement slab has landed
         cluster.sync();
 
         // ---- B: this CTA's columns: IFFT over the box rows -> modulus -> FFT -> box rows
@@ -164,11 +207,11 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
                 const int r = l + 32 * m;
                 x[m] = (r >= b0 && r < b0 + B) ? S[size_t(r - b0) * RS + jj] : make_float2(0.f, 0.f);
             }
-            F.template f1<true>(x);
+            F.f1(x);  // = conj(e), e the unscaled 2-D IFFT
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int row = k0 + M * brev5(l);
-                const float Iv = float(I_s[jj * IS + k0 * (NLR / M) + brev5(l)]);
+                const float Iv = float(I_s[row * SW + (jj ^ ((2 * brev5(l)) & (SW - 1)))]);
                 den += Iv;
                 // branch-free: |e|^2 at or below FLT_MIN counts as |e| = 0 (recon.cpp:122)
                 const float meas = sqrt_ftz(Iv);
@@ -180,9 +223,9 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
                 num = fmaf(dm, dm, num);
                 const float sc = nz ? meas * rr : 0.f;
                 const float z = nz ? 0.f : (((row + j) & 1) ? -meas : meas);
-                x[k0] = make_float2(fmaf(u.x, sc, z), u.y * sc);
+                x[k0] = make_float2(fmaf(u.x, sc, z), -u.y * sc);  // e' from u = conj(e)
             }
-            F.template f2<false>(x);
+            F.f2(x);
 #pragma unroll
             for (int r = 0; r < M; ++r) {
                 const int row = l + 32 * r;
@@ -199,6 +242,11 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
             wred[w * 4 + 1] = den;
         }
         cluster.sync();
+        if (e_next >= 0) {  // the slab is free: stage the next update's measurement under phase C
+            int itn, posn;
+            entry_at(e_next, itn, posn);
+            stage(posn);
+        }
 
         // ---- cluster-wide residual terms and EPRY maxima (fixed order: deterministic)
         if (w == 0) {
@@ -236,11 +284,12 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
                 const int col = l + 32 * m, owner = col / SW;
                 x[m] = cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)];
             }
-            F.template f1<false>(x);
+            F.f1(x);
+            const short2 run = SR[i];
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int c = k0 + M * brev5(l);
-                if (!sup[i * NLR + c]) continue;
+                if (c < run.x || c >= run.y) continue;
                 const float2 psi2 = cscale(x[k0], ((i + c) & 1) ? -1.f : 1.f);
                 float2* dst = cv + size_t(i) * NC + c;
                 float2* pp = pupil + i * NLR + c;
@@ -256,6 +305,7 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
             }
         }
         cluster.sync();  // slabs reusable; canvas and pupil writes visible to the whole cluster
+        e = e_next;
     }
     if (rank == 0) store_residuals(args, tile, stage_sum, G == 1);
 }

@@ -19,11 +19,6 @@ __device__ __forceinline__ float2 shfl_x(float2 v, int m) {
     return make_float2(__shfl_xor_sync(kFull, v.x, m), __shfl_xor_sync(kFull, v.y, m));
 }
 
-template <bool INV>
-__device__ __forceinline__ float2 tmul(float2 v, float2 w) {
-    return INV ? cmulc(v, w) : cmul(v, w);
-}
-
 template <bool INV, int M>
 __device__ __forceinline__ void dftM(float2 (&x)[M]) {
     if constexpr (M == 2) {
@@ -37,14 +32,16 @@ __device__ __forceinline__ void dftM(float2 (&x)[M]) {
     }
 }
 
-// Per-lane constants of the warp FFTs: cw[k] = W_(2h)^(l mod h) on the upper
-// lane of the stage h = 2^k (1 on the lower lane), sgk[k] = -1 on the upper
-// lane; tw[k0] = W_n^(l k0).
+// Per-lane constants of the warp FFTs, as (w, (-w.y, w.x)) pairs for the packed
+// two-instruction complex multiply: cw[k] = W_(2h)^(l mod h) on the upper lane
+// of the stage h = 2^k (1 on the lower lane), sgk[k] = -1 on the upper lane;
+// tw[k0] = W_n^(l k0). Forward transforms only: an inverse is run as
+// conj(FFT(conj x)), the conjugations folded into the callers' loads and stores.
 template <int M>
 struct WarpFFT {
-    float2 cw[5];
+    float4 cw[5];
     float sgk[5];
-    float2 tw[M];
+    float4 tw[M];
     __device__ void init(int l, int n) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
@@ -52,45 +49,44 @@ struct WarpFFT {
             const bool up = (l & h) != 0;
             double s, c;
             sincospi(-double(l & (h - 1)) / double(h), &s, &c);
-            cw[k] = up ? make_float2(float(c), float(s)) : make_float2(1.f, 0.f);
+            const float wc = up ? float(c) : 1.f, ws = up ? float(s) : 0.f;
+            cw[k] = make_float4(wc, ws, -ws, wc);
             sgk[k] = up ? -1.f : 1.f;
         }
 #pragma unroll
         for (int k0 = 0; k0 < M; ++k0) {
             double s, c;
             sincospi(-2.0 * double(l * k0) / double(n), &s, &c);
-            tw[k0] = make_float2(float(c), float(s));
+            tw[k0] = make_float4(float(c), float(s), -float(s), float(c));
         }
     }
-    template <bool INV>
+    static __device__ __forceinline__ float2 mul(float2 v, const float4& w) {
+        return cmul_sw(v, make_float2(w.x, w.y), make_float2(w.z, w.w));
+    }
+    // F1: x[l + 32 m] -> X[k0 + M br5(l)]: register DFT, twiddle, lane DIF
     __device__ __forceinline__ void f1(float2 (&x)[M]) const {
-        dftM<INV, M>(x);
+        dftM<false, M>(x);
 #pragma unroll
-        for (int k0 = 1; k0 < M; ++k0) x[k0] = tmul<INV>(x[k0], tw[k0]);
+        for (int k0 = 1; k0 < M; ++k0) x[k0] = mul(x[k0], tw[k0]);
 #pragma unroll
-        for (int k = 4; k >= 0; --k) {  // DIF: h = 16 .. 1
+        for (int k = 4; k >= 0; --k) {  // h = 16 .. 1
 #pragma unroll
-            for (int k0 = 0; k0 < M; ++k0) {
-                const float2 r = shfl_x(x[k0], 1 << k);
-                const float2 y = make_float2(fmaf(sgk[k], x[k0].x, r.x), fmaf(sgk[k], x[k0].y, r.y));
-                x[k0] = tmul<INV>(y, cw[k]);
-            }
+            for (int k0 = 0; k0 < M; ++k0) x[k0] = mul(cfma(sgk[k], x[k0], shfl_x(x[k0], 1 << k)), cw[k]);
         }
     }
-    template <bool INV>
+    // F2: x[k0 + M br5(l)] -> X[q + 32 r]: lane DIT, twiddle, register DFT
     __device__ __forceinline__ void f2(float2 (&x)[M]) const {
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {  // DIT: h = 1 .. 16
+        for (int k = 0; k < 5; ++k) {  // h = 1 .. 16
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
-                const float2 b = tmul<INV>(x[k0], cw[k]);
-                const float2 r = shfl_x(b, 1 << k);
-                x[k0] = make_float2(fmaf(sgk[k], b.x, r.x), fmaf(sgk[k], b.y, r.y));
+                const float2 b = mul(x[k0], cw[k]);
+                x[k0] = cfma(sgk[k], b, shfl_x(b, 1 << k));
             }
         }
 #pragma unroll
-        for (int k0 = 1; k0 < M; ++k0) x[k0] = tmul<INV>(x[k0], tw[k0]);
-        dftM<INV, M>(x);
+        for (int k0 = 1; k0 < M; ++k0) x[k0] = mul(x[k0], tw[k0]);
+        dftM<false, M>(x);
     }
 };
 
