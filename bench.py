@@ -305,8 +305,16 @@ def run_b200(args, W: Workload, rank, world):
                 traffic = json.load(open(tp)).get("dram_bytes_per_launch_config3")
             except (OSError, ValueError):
                 traffic = None
-        kernel = ("fpm_loop64 (fused per-LED update, 128-thread pair lattice, persistent over iters x LEDs)"
-                  if W.n == 64 else "fpm_loop_box (fused per-LED update, warp FFTs over the pupil box)")
+        cl = info["loop_ctas"] // max(info["num_tiles"], 1)
+        if cl > 1:
+            kernel = (f"fpm_loop_cluster (fused per-LED update, one tile over a {cl}-CTA cluster, DSMEM column "
+                      "slabs, warp FFTs over the pupil box)")
+        elif W.n == 64:
+            kernel = "fpm_loop64 (fused per-LED update, 128-thread pair lattice, persistent over iters x LEDs)"
+        else:
+            kernel = "fpm_loop_box (fused per-LED update, warp FFTs over the pupil box)"
+        # single-tile workloads cannot fill the GPU: also quote the roofline of the SMs they occupy
+        sms_used = min(sm_count, info["loop_ctas"])
         out = {"metric": W.metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f32 (complex64)", "data": "synthetic",
@@ -322,6 +330,8 @@ def run_b200(args, W: Workload, rank, world):
                                          "achieved_gbs": bytes_launch / (ms_loop / 1000.0) / 1e9,
                                          "peak_gbs": hbm_peak,
                                          "frac": bytes_launch / (ms_loop / 1000.0) / 1e9 / hbm_peak},
+                            "sms_used": sms_used,
+                            "frac_of_sms_used": achieved / (fp32_peak * sms_used / sm_count),
                             "loop_ms": ms_loop, "init_ms": ms_init, "finalize_ms": ms_fin,
                             "loop_share_of_step": ms_loop / ms},
                "clocks": clk.summary(),
