@@ -55,11 +55,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int NLR, int MODE, int NC, int CL, int NW>
-__global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args, const BoxArgs bx) {
+__global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cluster(const LoopArgs args, const BoxArgs bx) {
     constexpr int M = NLR / 32;
     constexpr int SW = NLR / CL;  // columns per CTA
     constexpr int RS = SW + 1;    // slab row stride (float2): column reads conflict-free
     constexpr int NT = NW * 32;
+    constexpr bool PF = M <= 4;  // register room to keep the next row's disk loads in flight
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = int(cluster.block_rank());
     const int tile = blockIdx.x / CL;
@@ -156,25 +157,54 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
         float2* cv = canvas + size_t(o.x) * NC + o.y;
 
         // ---- A: IFFT of this CTA's box rows, outputs to the column owners
+        // the disk loads of a warp's next row are issued before the current row's FFT
+        // (n <= 128; the n = 256 kernel has no register room for a second row)
         float omax = 0.f, pmax = 0.f;
-        for (int i = b0 + rank + CL * w; i < b0 + B; i += CL * NW) {
-            float2 x[M];
-            const short2 run = SR[i];
+        float2 Oa[M], Pa[M];
+        auto load_row = [&](int ii) {
+            const short2 run = SR[ii];
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int c = k0 + M * brev5(l);
-                float2 v = make_float2(0.f, 0.f);
-                if (c >= run.x && c < run.y) {
-                    const float2 O = cv[size_t(i) * NC + c];
-                    const float2 P = pupil[i * NLR + c];
-                    const float2 g = cmul(O, P);  // conj, signed: the row IFFT runs as conj(FFT(conj g))
-                    v = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
+                const bool on = c >= run.x && c < run.y;
+                Oa[k0] = on ? cv[size_t(ii) * NC + c] : make_float2(0.f, 0.f);
+                Pa[k0] = on ? pupil[ii * NLR + c] : make_float2(0.f, 0.f);
+            }
+        };
+        const int i0 = b0 + rank + CL * w;
+        if (PF && i0 < b0 + B) load_row(i0);
+        for (int i = i0; i < b0 + B; i += CL * NW) {
+            float2 x[M];
+            if constexpr (PF) {
+#pragma unroll
+                for (int k0 = 0; k0 < M; ++k0) {
+                    const int c = k0 + M * brev5(l);
+                    const float2 g = cmul(Oa[k0], Pa[k0]);  // conj, signed: the row IFFT runs as conj(FFT(conj g))
+                    x[k0] = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
                     if (MODE == kModeEPRY) {
-                        omax = fmaxf(omax, cabs2(O));
-                        pmax = fmaxf(pmax, cabs2(P));
+                        omax = fmaxf(omax, cabs2(Oa[k0]));
+                        pmax = fmaxf(pmax, cabs2(Pa[k0]));
                     }
                 }
-                x[k0] = v;
+                if (i + CL * NW < b0 + B) load_row(i + CL * NW);
+            } else {
+                const short2 run = SR[i];
+#pragma unroll
+                for (int k0 = 0; k0 < M; ++k0) {
+                    const int c = k0 + M * brev5(l);
+                    float2 v = make_float2(0.f, 0.f);
+                    if (c >= run.x && c < run.y) {
+                        const float2 O = cv[size_t(i) * NC + c];
+                        const float2 P = pupil[i * NLR + c];
+                        const float2 g = cmul(O, P);
+                        v = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
+                        if (MODE == kModeEPRY) {
+                            omax = fmaxf(omax, cabs2(O));
+                            pmax = fmaxf(pmax, cabs2(P));
+                        }
+                    }
+                    x[k0] = v;
+                }
             }
             F.f2(x);  // S keeps conj(IFFT_rows(g)): phase B's forward column FFT undoes it
 #pragma unroll
@@ -278,6 +308,18 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
 
         // ---- C: FFT of this CTA's box rows (fetched from the column slabs), scatter
         for (int i = b0 + rank + CL * w; i < b0 + B; i += CL * NW) {
+            // the scatter's disk operands are loaded first, their latency under the FFT
+            const short2 run = SR[i];
+            float2 Pc[PF ? M : 1], Oc[PF ? M : 1];
+            if constexpr (PF) {
+#pragma unroll
+                for (int k0 = 0; k0 < M; ++k0) {
+                    const int c = k0 + M * brev5(l);
+                    const bool on = c >= run.x && c < run.y;
+                    Pc[k0] = on ? pupil[i * NLR + c] : make_float2(0.f, 0.f);
+                    Oc[k0] = (MODE == kModeEPRY && on) ? cv[size_t(i) * NC + c] : make_float2(0.f, 0.f);
+                }
+            }
             float2 x[M];
 #pragma unroll
             for (int m = 0; m < M; ++m) {
@@ -285,7 +327,6 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
                 x[m] = cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)];
             }
             F.f1(x);
-            const short2 run = SR[i];
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int c = k0 + M * brev5(l);
@@ -293,11 +334,13 @@ __global__ void __launch_bounds__(NW * 32) fpm_loop_cluster(const LoopArgs args,
                 const float2 psi2 = cscale(x[k0], ((i + c) & 1) ? -1.f : 1.f);
                 float2* dst = cv + size_t(i) * NC + c;
                 float2* pp = pupil + i * NLR + c;
-                const float2 P = *pp;
+                float2 P;
+                if constexpr (PF) P = Pc[k0]; else P = *pp;
                 if (MODE == kModeGS) {
                     *dst = cmulc(psi2, P);
                 } else {
-                    const float2 O = *dst;
+                    float2 O;
+                    if constexpr (PF) O = Oc[k0]; else O = *dst;
                     const float2 d = csub(psi2, cmul(O, P));
                     if (inv_pmax > 0.f) *dst = cadd(O, cscale(cmulc(d, P), inv_pmax));
                     if (inv_omax > 0.f) *pp = cadd(P, cscale(cmulc(d, O), inv_omax));
