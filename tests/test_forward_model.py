@@ -1,0 +1,105 @@
+"""GPU forward model (paper_2203_02507_b200.forward)
+against the oracle's simulate_dataset (forward.cpp:172-282): same u16 frames.
+The CPU cases run the same torch code on the host; the GPU cases add a
+BASELINE-scale property check (simulate -> reconstruct -> compare)."""
+import numpy as np
+import pytest
+
+import paper_2203_02507_b200 as fpm
+from paper_2203_02507_b200.forward import simulate_dataset
+from tests.helpers import amp_phase_rel, gpu_cfg, orc_cfg
+
+CASES = [  # (tile, overlap, scan, fov, order, defocus)
+    (64, 8, 3, 64, "spiral", 0.0),
+    (64, 8, 5, 120, "spiral", 0.0),     # guard bands 0/32 -> 96-px crops, feathered overlap
+    (64, 8, 5, 121, "raster", 12.0),    # clamped last tile, odd guard, defocus CTF
+    (64, 0, 3, 128, "spiral", -5.0),
+    (128, 26, 3, 230, "spiral", 0.0),
+]
+
+
+def _frames_match(got, ref):
+    d = np.abs(got.astype(np.int64) - ref.astype(np.int64))
+    return d.max() <= 1 and np.count_nonzero(d) <= max(1, d.size // 100000)
+
+
+def _case(orc, tile, ov, scan, fov, order, dz, seed=3):
+    cfg = gpu_cfg(tile_size=tile, tile_overlap=ov, led_scan_rows=scan, led_scan_cols=scan)
+    oc = orc_cfg(cfg)
+    size = max(fov * 4, 256)
+    obj = orc.synth_object("composite", size, seed)[: fov * 4, : fov * 4]
+    seq = orc.led_sequence(order, oc)
+    return cfg, obj, seq, orc.simulate_dataset(obj, seq, oc, defocus_um=dz)
+
+
+@pytest.mark.parametrize("case", CASES[:4])
+def test_forward_model_matches_oracle_cpu(orc, case):
+    cfg, obj, seq, ref = _case(orc, *case)
+    got = simulate_dataset(obj, seq, cfg, defocus_um=case[5], device="cpu")
+    assert got.images.shape == ref.images.shape
+    assert _frames_match(got.images, ref.images)
+    assert [tuple(x) for x in got.leds] == [tuple(x) for x in ref.leds]
+    assert np.allclose(got.timestamps, ref.timestamps)
+
+
+def test_forward_model_errors_cpu():
+    cfg = gpu_cfg()
+    with pytest.raises(fpm.DataError, match="multiple of upsample"):
+        simulate_dataset(np.ones((258, 258), complex), [(32, 32)], cfg, device="cpu")
+    with pytest.raises(fpm.DataError, match="identically zero"):
+        simulate_dataset(np.zeros((256, 256), complex), [(32, 32)], cfg, device="cpu")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_forward_model_matches_oracle_gpu(orc, case):
+    cfg, obj, seq, ref = _case(orc, *case)
+    got = simulate_dataset(obj, seq, cfg, defocus_um=case[5], device="cuda")
+    assert _frames_match(got.images, ref.images)
+
+
+@pytest.mark.gpu
+def test_simulate_then_reconstruct_at_scale(orc):
+    """A 512-px FOV (64 tiles, 15x15 LEDs, the config-3 tile geometry) simulated
+    on the GPU, reconstructed on the GPU, against the oracle's reconstruction of
+    the same frames (1e-3, the north star's full-count bound) and the truth."""
+    cfg = fpm.OpticalConfig(tile_size=64, tile_overlap=0, upsample=4, led_scan_rows=15, led_scan_cols=15)
+    oc = orc_cfg(cfg)
+    obj = orc.synth_object("composite", 2048, 11)
+    seq = orc.led_sequence("spiral", oc)
+    fs = simulate_dataset(obj, seq, cfg, device="cuda")
+    assert fs.images.shape == (225, 512, 512)
+    opt = fpm.RunOptions(iters=3)
+    got = fpm.run_offline(fs, cfg, seq, opt, stitch=False)
+    ofs = orc.FrameStack(fs.images, list(fs.leds))
+    ref = orc.run_offline(ofs, oc, seq, 3, want_stitched=False, want_tiles=True)
+    for t in (0, 27, 63):
+        amp, ph = amp_phase_rel(got.tiles[t], ref.tiles[t])
+        assert amp < 1e-3 and ph < 1e-3, (t, amp, ph)
+
+
+@pytest.mark.gpu
+def test_config3_full_fov_physical_parity(orc):
+    """BASELINE config 3 at full size on physical data: a 2048x2048-sensor stack
+    (1,024 tiles, 15x15 LEDs, per-tile defocus) simulated on the GPU,
+    reconstructed with 10 EPRY iterations in one launch; a corner, an edge and an
+    interior tile against the oracle's reconstruct_tile of the same frames
+    (north-star check 3: <= 1e-3 after the full count)."""
+    cfg = fpm.OpticalConfig(tile_size=64, tile_overlap=0, upsample=4, led_scan_rows=15, led_scan_cols=15)
+    oc = orc_cfg(cfg)
+    obj = orc.synth_object("composite", 8192, 21)
+    seq = orc.led_sequence("spiral", oc)
+    fs = simulate_dataset(obj, seq, cfg, defocus_um=6.0, device="cuda")
+    assert fs.images.shape == (225, 2048, 2048)
+    T = 1024
+    rng = np.random.default_rng(7)
+    defocus = rng.uniform(-10, 10, T)
+    opt = fpm.RunOptions(iters=10, mode="epry", tile_defocus_um=list(defocus))
+    got = fpm.run_offline(fs, cfg, seq, opt, stitch=False)
+    assert got.tiles.shape == (T, 256, 256)
+    ofs = orc.FrameStack(fs.images, list(fs.leds))
+    for t in (0, 31, 528):
+        ref = orc.reconstruct_tile(ofs, oc, 10, seq, tile_index=t, mode="epry", tile_defocus=float(defocus[t]))
+        amp, ph = amp_phase_rel(got.tiles[t], ref.hr)
+        assert amp < 1e-3 and ph < 1e-3, (t, amp, ph)
+        assert np.allclose(got.tile_metrics[t].pass_mean_residual, ref.residuals, rtol=1e-3)
