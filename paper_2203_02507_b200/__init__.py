@@ -12,4 +12,6 @@ from .engine import (ConfigError, DataError, DomainError, Engine, FrameSet, Opti
                      reconstruct_request, reconstruct_tile, run_offline, run_online, scan_leds, select_tiles, sequence_offsets,
                      spectrum_offset_px, stitch_mosaic, synthesized_na, tile_origins, update_step)
 
+from .forward import simulate_dataset  # noqa: F401,E402
+
 __all__ = [n for n in dir() if not n.startswith("_")]
