@@ -5,13 +5,16 @@ px (overlap 0), 15x15 LEDs (spiral order), 10 iterations EPRY, per-tile
 illumination k-vectors and per-tile defocus pupils (uniform +-10 um, seed 7);
 synthetic u16 LR stack (uniform [0, 52428], seed 1: the cost is
 data-independent). One step = one full reconstruction (pupils + init_canvas +
-LED loop + canvas_to_field) of every tile. Under torchrun the tiles are
-sharded in contiguous tile-row bands over the ranks (strong scaling, config
-4); each rank holds only its band of the stack; the HR tiles are gathered to
-rank 0 (the only inter-GPU step).
+LED loop + canvas_to_field) of every tile. Under torchrun (N > 1) the
+default is weak scaling: tiles are independent units, so every
+rank reconstructs its own full config-3 FOV (its own synthetic stack) with no
+collective in the step, and `value` = all ranks' updates / the slowest rank's
+time. `--scaling strong` runs BASELINE config 4 instead: one FOV sharded in
+contiguous tile-row bands over the ranks, each holding only its band of the
+stack, the HR tiles gathered to rank 0 by NCCL (the only inter-GPU step).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--config 3|1|2|5] [--no-e2e] [--no-cpu]
+                  [--config 3|1|2|5] [--scaling weak|strong] [--no-e2e] [--no-cpu]
 
 `--config` 1/2/5 measure the other BASELINE shapes (single 64 px tile GS;
 single 128 px tile EPRY; 4096x4096 sensor of 256 px tiles, 21x21 LEDs).
@@ -197,7 +200,8 @@ def run_reference(args, W: Workload, rank, world):
     v = float(np.mean(rates))
     line = {"impl": "reference", "metric": W.metric, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * T * len(seq) / v,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": config_block(W, 1, {"parallelism": f"cpu x{cores} threads (tile pool, parallel.cpp:126-140)"}),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": cpu_sample_desc(W, T, cores)},
@@ -225,8 +229,9 @@ def run_b200(args, W: Workload, rank, world):
     L = len(seq)
     full = fpm.Request(cfg, W.iters, xy_all, of_all, np.arange(L, dtype=np.int32), 0, L, W.fov, W.fov, mode=W.mode,
                        tile_defocus_um=defocus_all)
-    shards = [shard_request(full, r, world) for r in range(world)]
-    me = shards[rank]
+    strong = args.scaling == "strong" and world > 1
+    shards = [shard_request(full, r, world) for r in range(world)] if strong else None
+    me = shards[rank] if strong else shard_request(full, 0, 1)
     T, H = len(me.tiles), me.y_hi - me.y_lo
     eng = fpm.Engine(local)
     plan = fpm.Plan(me.request, eng)
@@ -243,13 +248,14 @@ def run_b200(args, W: Workload, rank, world):
     resid = torch.empty((T, W.iters), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     mosaic_tiles = torch.empty((len(xy_all), N, N, 2), dtype=torch.float32, device=dev) if (
-        world > 1 and rank == 0) else None
-    flush = l2_flush_needed(W, world)
+        strong and rank == 0) else None
+    share = world if strong else 1  # ranks sharing one FOV's stack
+    flush = l2_flush_needed(W, share)
     scrub = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev) if flush else None
 
     def step():
         plan.execute(frames.data_ptr(), W.fov, hr.data_ptr(), resid.data_ptr(), None, stream.cuda_stream)
-        if world > 1:  # the only inter-GPU step: HR tiles gathered to rank 0 (NCCL send/recv)
+        if strong:  # the only inter-GPU step: HR tiles gathered to rank 0 (NCCL send/recv)
             gather_tiles(hr, shards, rank, mosaic_tiles.shape if rank == 0 else None, out=mosaic_tiles)
 
     for _ in range(args.warmup):
@@ -284,7 +290,13 @@ def run_b200(args, W: Workload, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ok = bool(torch.isfinite(resid).all().item())
-    value = W.updates / (ms / 1000.0)
+    units = W.updates * (1 if strong else world)  # weak: every rank ran the full workload
+    value = units / (ms / 1000.0)
+
+    # e2e through the host-buffer C-ABI call: every rank (weak scaling: each its own FOV)
+    e2e = None
+    if not args.no_e2e and not strong:
+        e2e = e2e_leg(args, W, cfg, seq, xy_all, of_all, defocus_all, eng, world)
 
     out = None
     if rank == 0:
@@ -316,10 +328,13 @@ def run_b200(args, W: Workload, rank, world):
         # single-tile workloads cannot fill the GPU: also quote the roofline of the SMs they occupy
         sms_used = min(sm_count, info["loop_ctas"])
         out = {"metric": W.metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "strong" if strong else "weak",
                "vs_baseline": None, "dtype": "f32 (complex64)", "data": "synthetic",
-               "config": config_block(W, world, {"parallelism": f"tile-shard x{world}" if world > 1
-                                                 else "tiles->CTAs, 1 GPU", "full_recon_s": ms / 1000.0}),
+               "config": config_block(W, share, {
+                   "parallelism": (f"tile-row bands x{world} + NCCL HR gather (config 4)" if strong else
+                                   f"one independent FOV per GPU x{world}" if world > 1 else "tiles->CTAs, 1 GPU"),
+                   "updates_per_step_all_ranks": units, "full_recon_s": ms / 1000.0}),
                "roofline": {"kernel": kernel, "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
                             "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": traffic,
                             "peak_source": f"nominal FP32: {sm_count} SMs x 128 FMA lanes x 2 x {sm_max:.0f} MHz "
@@ -337,8 +352,8 @@ def run_b200(args, W: Workload, rank, world):
                "clocks": clk.summary(),
                "gpu_launches": info["launches_per_execute"] * args.steps,
                "residuals_finite": ok}
-        if not args.no_e2e and world == 1:
-            out["e2e"] = e2e_leg(args, W, cfg, seq, xy_all, of_all, defocus_all, eng)
+        if e2e is not None:
+            out["e2e"] = e2e
         if world == 1 and not args.no_cpu:
             cores = os.cpu_count() or 1
             rate, wall, Tc = cpu_sample(W, cfg, seq, cores)
@@ -351,9 +366,11 @@ def run_b200(args, W: Workload, rank, world):
     return 0
 
 
-def e2e_leg(args, W: Workload, cfg, seq, xy, of, defocus, eng):
+def e2e_leg(args, W: Workload, cfg, seq, xy, of, defocus, eng, world: int = 1):
     """Same metric through the reference-facing host-buffer call (fpmgpu_reconstruct_tiles):
-    pinned host LR stack -> H2D -> reconstruct -> D2H of HR tiles + residuals, every step."""
+    pinned host LR stack -> H2D -> reconstruct -> D2H of HR tiles + residuals, every step.
+    With N ranks (weak scaling) every rank times its own FOV; the slowest rank's wall
+    time over the steps counts, and value = all ranks' updates / that time."""
     import ctypes as C
 
     import torch
@@ -379,15 +396,23 @@ def e2e_leg(args, W: Workload, cfg, seq, xy, of, defocus, eng):
 
     for _ in range(max(1, args.warmup)):
         call()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         call()
     wall = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        t = torch.tensor([wall], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
     del keep
-    return {"value": W.updates / wall, "unit": UNIT, "ms_per_step": wall * 1000.0,
-            "h2d_bytes_per_step": int(host.numel() * 2),
-            "d2h_bytes_per_step": int(hr_host.numel() * 4 + res_host.numel() * 8),
-            "path": "fpmgpu_reconstruct_tiles (host buffers, pinned), wall clock around the synchronous call"}
+    return {"value": world * W.updates / wall, "unit": UNIT, "ms_per_step": wall * 1000.0,
+            "h2d_bytes_per_step": int(host.numel() * 2) * world,
+            "d2h_bytes_per_step": int(hr_host.numel() * 4 + res_host.numel() * 8) * world,
+            "path": "fpmgpu_reconstruct_tiles (host buffers, pinned), wall clock around the synchronous call"
+                    + (f", {world} ranks, max over ranks" if world > 1 else "")}
 
 
 def main():
@@ -397,6 +422,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", type=int, choices=sorted(WORKLOADS), default=3)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
