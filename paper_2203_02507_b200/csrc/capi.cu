@@ -173,6 +173,7 @@ int cluster_choice(int n, int N, int T) {
         return c;
     }
     if (n == 256 && N == 1024) return 4;
+    if (n == 128 && N == 512 && T * 16 <= 148) return 16;  // single-tile latency (config 2)
     if (n == 128 && N == 512 && T * 8 <= 148) return 8;
     return 0;
 }

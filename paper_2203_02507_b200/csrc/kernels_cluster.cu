@@ -359,6 +359,10 @@ cudaError_t launch_cluster_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStr
     auto k = fpm_loop_cluster<NLR, MODE, NC, CL, NW>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
+    if (CL > 8) {  // 16-CTA clusters are a non-portable size on sm_100
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(T * CL));
     cfg.blockDim = dim3(NW * 32);
@@ -376,11 +380,11 @@ cudaError_t launch_cluster_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStr
 
 }  // namespace
 
-int cluster_warps(int n, int cl) { return n == 64 ? 4 : (n == 256 && cl == 2) ? 16 : 8; }
+int cluster_warps(int n, int cl) { return (n == 64 || cl == 16) ? 4 : (n == 256 && cl == 2) ? 16 : 8; }
 
 bool cluster_supported(int n, int N, int cl) {
     if (n == 64) return N == 256 && (cl == 4 || cl == 8);
-    if (n == 128) return N == 512 && (cl == 2 || cl == 4 || cl == 8);
+    if (n == 128) return N == 512 && (cl == 2 || cl == 4 || cl == 8 || cl == 16);
     if (n == 256) return N == 1024 && (cl == 2 || cl == 4 || cl == 8);
     return false;
 }
@@ -396,6 +400,7 @@ cudaError_t launch_loop_cluster(int n, int mode, int cl, const LoopArgs& a, cons
     FPM_CL_CASE(128, 512, 2, 8)
     FPM_CL_CASE(128, 512, 4, 8)
     FPM_CL_CASE(128, 512, 8, 8)
+    FPM_CL_CASE(128, 512, 16, 4)
     FPM_CL_CASE(256, 1024, 2, 16)
     FPM_CL_CASE(256, 1024, 4, 8)
     FPM_CL_CASE(256, 1024, 8, 8)
