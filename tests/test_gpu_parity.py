@@ -308,7 +308,7 @@ def test_banded_host_path_bit_identical(eng, monkeypatch, bands):
         assert np.array_equal(pa, pb)
 
 
-@pytest.mark.parametrize("n,cl,mode", [(128, 2, "epry"), (128, 4, "gs"), (128, 8, "epry"), (256, 2, "gs"),
+@pytest.mark.parametrize("n,cl,mode", [(128, 2, "epry"), (128, 4, "gs"), (128, 8, "epry"), (128, 16, "gs"), (256, 2, "gs"),
                                        (256, 4, "epry"), (256, 8, "gs")])
 def test_cluster_kernel_matches_box_kernel(eng, monkeypatch, n, cl, mode):
     """A tile split over a CTA cluster (DSMEM column slabs) runs the box kernel's
