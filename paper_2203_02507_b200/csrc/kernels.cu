@@ -37,6 +37,9 @@ constexpr int kIBytes = 64 * 64 * 2;            // staged u16 measurement, TMA 1
 constexpr int kTBytes = 64 * 64 * 8;            // transpose buffer (swizzled, unpadded)
 constexpr int kGroupBytes = kIBytes + kTBytes;  // 40 KB, a multiple of 1 KB
 constexpr int kGroupThreads = 128;
+#ifndef FPM_PASS_UNROLL
+#define FPM_PASS_UNROLL 1  // two specialised FFT bodies (pruning resolved at compile time); 0: one rolled body
+#endif
 #ifndef FPM_LOOP_MINB
 #define FPM_LOOP_MINB 4  // resident tiles per SM the register budget is sized for
 #endif
@@ -349,7 +352,11 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
             //      run as conj(FFT(conj x)); modulus replacement
             // ---- pass 1: centered forward transform of the corrected field
             float inv_omax = 0.f, inv_pmax = 0.f;
+#if FPM_PASS_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
             for (int pass = 0; pass < 2; ++pass) {
             fft64x64_fwd_rt(v, T_s, W4_s, p, h, sg, tw, twsw, g, PRUNE && pass == 0, PRUNE && pass == 1);
             if (pass == 1) break;
