@@ -126,6 +126,16 @@ int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* re
                              const uint16_t* frames, int64_t row_pitch, float* hr,
                              double* residuals, float* pupils_out, int* lag_used);
 
+/* The same call split in two, so consecutive requests overlap: request k + 1's
+ * LR upload runs under request k's reconstruction (two staging slots per
+ * context; a third submit first waits for the oldest). The host buffers of a
+ * request must stay valid and untouched until fpmgpu_wait(ticket) returns;
+ * use pinned memory for the copies to be asynchronous. */
+int fpmgpu_reconstruct_tiles_async(fpmgpu_context* ctx, const fpmgpu_recon_request* req,
+                                   const uint16_t* frames, int64_t row_pitch, float* hr,
+                                   double* residuals, float* pupils_out, long long* ticket);
+int fpmgpu_wait(fpmgpu_context* ctx, long long ticket, int* lag_used);
+
 /* Online session — replaces run_online (parallel.cpp:198-317): frames arrive one
  * at a time; each is copied to the device on arrival, and the first-pass
  * update of sequence position k is launched for every tile as soon as frames

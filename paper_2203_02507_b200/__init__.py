@@ -9,7 +9,7 @@ from .engine import (ConfigError, DataError, DomainError, Engine, FrameSet, Opti
                      UnsafeLagError, build_pupil, build_schedule, canvas_to_field, crop_frame, default_engine,
                      illumination_wavevector, init_canvas, led_sequence, make_request, min_safe_lag,
                      min_safe_lag_tile, partition_arrays, partition_tiles, pipelined_reconstruct_tile,
-                     reconstruct_request, reconstruct_tile, run_offline, run_online, scan_leds, select_tiles, sequence_offsets,
+                     reconstruct_request, reconstruct_request_async, reconstruct_tile, run_offline, run_online, scan_leds, select_tiles, sequence_offsets,
                      spectrum_offset_px, stitch_mosaic, synthesized_na, tile_origins, update_step)
 
 from .forward import simulate_dataset  # noqa: F401,E402

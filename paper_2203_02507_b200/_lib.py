@@ -104,6 +104,7 @@ EXPORTS = [
     "fpmgpu_plan_destroy", "fpmgpu_plan_get_info", "fpmgpu_plan_phase_times", "fpmgpu_update_step", "fpmgpu_init_canvas",
     "fpmgpu_canvas_to_field", "fpmgpu_stitch_mosaic", "fpmgpu_stitch_mosaic_device",
     "fpmgpu_online_begin", "fpmgpu_online_push", "fpmgpu_online_finish", "fpmgpu_online_destroy",
+    "fpmgpu_reconstruct_tiles_async", "fpmgpu_wait",
 ]
 
 _lib: C.CDLL | None = None
@@ -123,6 +124,9 @@ def lib() -> C.CDLL:
         L.fpmgpu_reconstruct_tiles.argtypes = [C.c_void_p, C.POINTER(ReconRequestC), C.c_void_p, C.c_int64,
                                                C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
         L.fpmgpu_plan_create.argtypes = [C.c_void_p, C.POINTER(ReconRequestC), C.POINTER(C.c_void_p)]
+        L.fpmgpu_reconstruct_tiles_async.argtypes = [C.c_void_p, C.POINTER(ReconRequestC), C.c_void_p, C.c_int64,
+                                                     C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_longlong)]
+        L.fpmgpu_wait.argtypes = [C.c_void_p, C.c_longlong, C.POINTER(C.c_int)]
         L.fpmgpu_online_begin.argtypes = [C.c_void_p, C.POINTER(ReconRequestC), C.POINTER(C.c_void_p)]
         L.fpmgpu_online_push.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int)]
         L.fpmgpu_online_finish.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]

@@ -189,23 +189,32 @@ std::vector<float2> twiddles(int N) {
 
 }  // namespace
 
-struct fpmgpu_context {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    DevBuf<float2> tw256, tw512, tw1024;
-    // host-path staging
+// One in-flight host-buffer request: device staging, one cached plan per tile
+// band (band b = tiles [band_t0[b], band_t0[b+1])), a stream per band.
+struct HostSlot {
     DevBuf<uint16_t> frames;
     DevBuf<float2> hr;
     DevBuf<double> resid;
     DevBuf<float2> pup;
-    // host path: one cached plan per tile band, band b = tiles [band_t0[b], band_t0[b+1])
-    std::vector<fpmgpu_plan*> cached;
+    std::vector<fpmgpu_plan*> plans;
     std::vector<int> band_t0;
-    std::vector<cudaStream_t> band_streams;
-    std::vector<cudaEvent_t> band_events;
-    std::vector<int> cached_key_i;
-    std::vector<double> cached_key_d;
-    std::vector<float> cached_key_f;
+    std::vector<cudaStream_t> streams;
+    std::vector<cudaEvent_t> arrived;  // band's LR rows on the device (recorded on the copy stream)
+    std::vector<cudaEvent_t> done;     // band's outputs back on the host
+    std::vector<int> key_i;
+    std::vector<double> key_d;
+    std::vector<float> key_f;
+    long long ticket = -1;  // request in flight, -1 = idle
+    int lag = 0;
+};
+
+struct fpmgpu_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;  // copy stream of the host path; plan uploads
+    DevBuf<float2> tw256, tw512, tw1024;
+    // host path: two slots, so request k + 1's upload overlaps request k's reconstruction
+    HostSlot slots[2];
+    long long next_ticket = 0;
 
     const float2* twiddle_table(int N) {
         DevBuf<float2>* b = N == 256 ? &tw256 : N == 512 ? &tw512 : N == 1024 ? &tw1024 : nullptr;
@@ -496,7 +505,7 @@ void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* 
                            cudaMemcpyDeviceToDevice, s), "pupil out");
 }
 
-bool same_request(const fpmgpu_context& c, const fpmgpu_recon_request& r, std::vector<int>& ki,
+bool same_request(const HostSlot& c, const fpmgpu_recon_request& r, std::vector<int>& ki,
                   std::vector<double>& kd, std::vector<float>& kf) {
     ki.clear();
     kd.clear();
@@ -512,7 +521,7 @@ bool same_request(const fpmgpu_context& c, const fpmgpu_recon_request& r, std::v
     kd.push_back(r.beta);
     if (r.tile_defocus_um) kd.insert(kd.end(), r.tile_defocus_um, r.tile_defocus_um + r.num_tiles);
     if (r.pupils) kf.insert(kf.end(), r.pupils, r.pupils + 2 * size_t(r.num_tiles) * r.cfg.tile_size * r.cfg.tile_size);
-    return !c.cached.empty() && ki == c.cached_key_i && kd == c.cached_key_d && kf == c.cached_key_f;
+    return !c.plans.empty() && ki == c.key_i && kd == c.key_d && kf == c.key_f;
 }
 
 }  // namespace
@@ -817,12 +826,15 @@ int fpmgpu_destroy(fpmgpu_context* ctx) {
     return guarded([&] {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
-        for (auto* p : ctx->cached) delete p;
-        for (auto s : ctx->band_streams) {
-            cudaStreamSynchronize(s);
-            cudaStreamDestroy(s);
+        for (auto& sl : ctx->slots) {
+            for (auto st : sl.streams) {
+                cudaStreamSynchronize(st);
+                cudaStreamDestroy(st);
+            }
+            for (auto* p : sl.plans) delete p;
+            for (auto e : sl.arrived) cudaEventDestroy(e);
+            for (auto e : sl.done) cudaEventDestroy(e);
         }
-        for (auto e : ctx->band_events) cudaEventDestroy(e);
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
@@ -922,108 +934,153 @@ std::vector<int> host_bands(const fpmgpu_recon_request& r) {
 
 }  // namespace
 
-int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames,
-                             int64_t row_pitch, float* hr, double* residuals, float* pupils_out, int* lag_used) {
+namespace {
+
+void wait_slot(HostSlot& sl) {
+    if (sl.ticket < 0) return;
+    for (auto e : sl.done) ck(cudaEventSynchronize(e), "reconstruct");
+    sl.ticket = -1;
+}
+
+// Enqueue one host-buffer reconstruction on slot `sl` (returns before it completes).
+void submit(fpmgpu_context* ctx, HostSlot& sl, const fpmgpu_recon_request* req, const uint16_t* frames,
+            int64_t row_pitch, float* hr, double* residuals, float* pupils_out) {
+    cudaStream_t s = ctx->stream;
+    std::vector<int> ki;
+    std::vector<double> kd;
+    std::vector<float> kf;
+    const std::vector<int> t0 = host_bands(*req);
+    const int B = int(t0.size()) - 1;
+    const bool hit = same_request(sl, *req, ki, kd, kf) && sl.band_t0 == t0;
+    if (!hit) {
+        for (auto* q : sl.plans) delete q;
+        sl.plans.clear();
+        sl.band_t0.clear();
+        for (int b = 0; b < B; ++b) {
+            // band b: the same request over tiles [t0[b], t0[b+1])
+            fpmgpu_recon_request rb = *req;
+            const int a = t0[b], cnt = t0[b + 1] - t0[b];
+            rb.num_tiles = cnt;
+            rb.tile_xy = req->tile_xy + 2 * size_t(a);
+            rb.offsets = req->offsets + 2 * size_t(a) * req->num_leds;
+            if (req->tile_defocus_um) rb.tile_defocus_um = req->tile_defocus_um + a;
+            if (req->pupils) rb.pupils = req->pupils + 2 * size_t(a) * req->cfg.tile_size * req->cfg.tile_size;
+            auto p = std::make_unique<fpmgpu_plan>();
+            p->ctx = ctx;
+            build_plan(*p, rb);
+            sl.plans.push_back(p.release());
+        }
+        sl.band_t0 = t0;
+        sl.key_i.swap(ki);
+        sl.key_d.swap(kd);
+        sl.key_f.swap(kf);
+    }
+    while (int(sl.streams.size()) < B) {
+        cudaStream_t bs;
+        cudaEvent_t e0, e1;
+        ck(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "event");
+        sl.streams.push_back(bs);
+        sl.arrived.push_back(e0);
+        sl.done.push_back(e1);
+    }
+    const fpmgpu_plan& p0 = *sl.plans[0];
+    const int W = req->width, H = req->height, F = req->num_frames, T = req->num_tiles;
+    const int n = p0.n, N = p0.N, iters = req->iters;
+    const int64_t pitch = (int64_t(W) + 63) / 64 * 64;
+    uint16_t* fd = sl.frames.ensure(size_t(F) * H * pitch);
+    const size_t hr_n = size_t(T) * N * N, pup_n = size_t(T) * n * n;
+    float2* hr_d = hr ? sl.hr.ensure(hr_n) : nullptr;
+    double* res_d = sl.resid.ensure(size_t(T) * iters);
+    float2* pup_d = pupils_out ? sl.pup.ensure(pup_n) : nullptr;
+    ctx->twiddle_table(N);  // its one-time upload must precede the band events on s
+    // frame rows [lo, hi) of every frame: one pitched 3-D copy (x bytes, rows, frames)
+    auto copy_rows = [&](int lo, int hi) {
+        if (hi <= lo) return;
+        cudaMemcpy3DParms m{};
+        m.srcPtr = make_cudaPitchedPtr(const_cast<uint16_t*>(frames), size_t(row_pitch) * 2, size_t(W) * 2, H);
+        m.dstPtr = make_cudaPitchedPtr(fd, size_t(pitch) * 2, size_t(W) * 2, H);
+        m.srcPos = make_cudaPos(0, size_t(lo), 0);
+        m.dstPos = make_cudaPos(0, size_t(lo), 0);
+        m.extent = make_cudaExtent(size_t(W) * 2, size_t(hi - lo), size_t(F));
+        m.kind = cudaMemcpyHostToDevice;
+        ck(cudaMemcpy3DAsync(&m, s), "frames H2D");
+    };
+    int clo = 0, chi = 0;  // rows already on the device: [clo, chi)
+    for (int b = 0; b < B; ++b) {
+        int y0 = H, y1 = 0;
+        for (int t = t0[b]; t < t0[b + 1]; ++t) {
+            y0 = std::min(y0, req->tile_xy[2 * t + 1]);
+            y1 = std::max(y1, req->tile_xy[2 * t + 1] + n);
+        }
+        if (chi <= clo) {
+            copy_rows(y0, y1);
+            clo = y0;
+            chi = y1;
+        } else {
+            copy_rows(std::min(y0, clo), clo);
+            copy_rows(chi, std::max(y1, chi));
+            clo = std::min(y0, clo);
+            chi = std::max(y1, chi);
+        }
+        cudaStream_t bs = sl.streams[b];
+        ck(cudaEventRecord(sl.arrived[b], s), "event");
+        ck(cudaStreamWaitEvent(bs, sl.arrived[b], 0), "wait");
+        fpmgpu_plan& pb = *sl.plans[b];
+        const size_t a = size_t(t0[b]), cnt = size_t(t0[b + 1] - t0[b]);
+        execute_plan(pb, fd, pitch, hr_d ? reinterpret_cast<float*>(hr_d + a * N * N) : nullptr, res_d + a * iters,
+                     pup_d ? reinterpret_cast<float*>(pup_d + a * n * n) : nullptr, bs);
+        if (hr)
+            ck(cudaMemcpyAsync(hr + 2 * a * N * N, hr_d + a * N * N, cnt * N * N * sizeof(float2),
+                               cudaMemcpyDeviceToHost, bs), "hr D2H");
+        if (residuals)
+            ck(cudaMemcpyAsync(residuals + a * iters, res_d + a * iters, sizeof(double) * cnt * iters,
+                               cudaMemcpyDeviceToHost, bs), "residual D2H");
+        if (pupils_out)
+            ck(cudaMemcpyAsync(pupils_out + 2 * a * n * n, pup_d + a * n * n, cnt * n * n * sizeof(float2),
+                               cudaMemcpyDeviceToHost, bs), "pupil D2H");
+        ck(cudaEventRecord(sl.done[b], bs), "event");
+    }
+    sl.lag = p0.lag;
+}
+
+// the slot a new request goes to: request k uses slot k mod 2 (waiting for k - 2)
+HostSlot& slot_for(fpmgpu_context* ctx, long long ticket) { return ctx->slots[ticket & 1]; }
+
+}  // namespace
+
+int fpmgpu_reconstruct_tiles_async(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames,
+                                   int64_t row_pitch, float* hr, double* residuals, float* pupils_out,
+                                   long long* ticket) {
     return guarded([&] {
         ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-        cudaStream_t s = ctx->stream;
-        std::vector<int> ki;
-        std::vector<double> kd;
-        std::vector<float> kf;
-        const std::vector<int> t0 = host_bands(*req);
-        const int B = int(t0.size()) - 1;
-        const bool hit = same_request(*ctx, *req, ki, kd, kf) && ctx->band_t0 == t0;
-        if (!hit) {
-            for (auto* q : ctx->cached) delete q;
-            ctx->cached.clear();
-            ctx->band_t0.clear();
-            for (int b = 0; b < B; ++b) {
-                // band b: the same request over tiles [t0[b], t0[b+1])
-                fpmgpu_recon_request rb = *req;
-                const int a = t0[b], cnt = t0[b + 1] - t0[b];
-                rb.num_tiles = cnt;
-                rb.tile_xy = req->tile_xy + 2 * size_t(a);
-                rb.offsets = req->offsets + 2 * size_t(a) * req->num_leds;
-                if (req->tile_defocus_um) rb.tile_defocus_um = req->tile_defocus_um + a;
-                if (req->pupils) rb.pupils = req->pupils + 2 * size_t(a) * req->cfg.tile_size * req->cfg.tile_size;
-                auto p = std::make_unique<fpmgpu_plan>();
-                p->ctx = ctx;
-                build_plan(*p, rb);
-                ctx->cached.push_back(p.release());
-            }
-            ctx->band_t0 = t0;
-            ctx->cached_key_i.swap(ki);
-            ctx->cached_key_d.swap(kd);
-            ctx->cached_key_f.swap(kf);
-        }
-        while (int(ctx->band_streams.size()) < B) {
-            cudaStream_t bs;
-            cudaEvent_t be;
-            ck(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking), "stream");
-            ck(cudaEventCreateWithFlags(&be, cudaEventDisableTiming), "event");
-            ctx->band_streams.push_back(bs);
-            ctx->band_events.push_back(be);
-        }
-        const fpmgpu_plan& p0 = *ctx->cached[0];
-        const int W = req->width, H = req->height, F = req->num_frames, T = req->num_tiles;
-        const int n = p0.n, N = p0.N, iters = req->iters;
-        const int64_t pitch = (int64_t(W) + 63) / 64 * 64;
-        uint16_t* fd = ctx->frames.ensure(size_t(F) * H * pitch);
-        const size_t hr_n = size_t(T) * N * N, pup_n = size_t(T) * n * n;
-        float2* hr_d = hr ? ctx->hr.ensure(hr_n) : nullptr;
-        double* res_d = ctx->resid.ensure(size_t(T) * iters);
-        float2* pup_d = pupils_out ? ctx->pup.ensure(pup_n) : nullptr;
-        ctx->twiddle_table(N);  // its one-time upload must precede the band events on s
-        // frame rows [lo, hi) of every frame: one pitched 3-D copy (x bytes, rows, frames)
-        auto copy_rows = [&](int lo, int hi) {
-            if (hi <= lo) return;
-            cudaMemcpy3DParms m{};
-            m.srcPtr = make_cudaPitchedPtr(const_cast<uint16_t*>(frames), size_t(row_pitch) * 2, size_t(W) * 2, H);
-            m.dstPtr = make_cudaPitchedPtr(fd, size_t(pitch) * 2, size_t(W) * 2, H);
-            m.srcPos = make_cudaPos(0, size_t(lo), 0);
-            m.dstPos = make_cudaPos(0, size_t(lo), 0);
-            m.extent = make_cudaExtent(size_t(W) * 2, size_t(hi - lo), size_t(F));
-            m.kind = cudaMemcpyHostToDevice;
-            ck(cudaMemcpy3DAsync(&m, s), "frames H2D");
-        };
-        int clo = 0, chi = 0;  // rows already on the device: [clo, chi)
-        for (int b = 0; b < B; ++b) {
-            int y0 = H, y1 = 0;
-            for (int t = t0[b]; t < t0[b + 1]; ++t) {
-                y0 = std::min(y0, req->tile_xy[2 * t + 1]);
-                y1 = std::max(y1, req->tile_xy[2 * t + 1] + n);
-            }
-            if (chi <= clo) {
-                copy_rows(y0, y1);
-                clo = y0;
-                chi = y1;
-            } else {
-                copy_rows(std::min(y0, clo), clo);
-                copy_rows(chi, std::max(y1, chi));
-                clo = std::min(y0, clo);
-                chi = std::max(y1, chi);
-            }
-            cudaStream_t bs = ctx->band_streams[b];
-            ck(cudaEventRecord(ctx->band_events[b], s), "event");
-            ck(cudaStreamWaitEvent(bs, ctx->band_events[b], 0), "wait");
-            fpmgpu_plan& pb = *ctx->cached[b];
-            const size_t a = size_t(t0[b]), cnt = size_t(t0[b + 1] - t0[b]);
-            execute_plan(pb, fd, pitch, hr_d ? reinterpret_cast<float*>(hr_d + a * N * N) : nullptr, res_d + a * iters,
-                         pup_d ? reinterpret_cast<float*>(pup_d + a * n * n) : nullptr, bs);
-            if (hr)
-                ck(cudaMemcpyAsync(hr + 2 * a * N * N, hr_d + a * N * N, cnt * N * N * sizeof(float2),
-                                   cudaMemcpyDeviceToHost, bs), "hr D2H");
-            if (residuals)
-                ck(cudaMemcpyAsync(residuals + a * iters, res_d + a * iters, sizeof(double) * cnt * iters,
-                                   cudaMemcpyDeviceToHost, bs), "residual D2H");
-            if (pupils_out)
-                ck(cudaMemcpyAsync(pupils_out + 2 * a * n * n, pup_d + a * n * n, cnt * n * n * sizeof(float2),
-                                   cudaMemcpyDeviceToHost, bs), "pupil D2H");
-        }
-        for (int b = 0; b < B; ++b) ck(cudaStreamSynchronize(ctx->band_streams[b]), "reconstruct");
-        ck(cudaStreamSynchronize(s), "reconstruct");
-        if (lag_used) *lag_used = p0.lag;
+        const long long t = ctx->next_ticket;
+        HostSlot& sl = slot_for(ctx, t);
+        wait_slot(sl);  // its buffers and plans are free once request t - 2 is done
+        submit(ctx, sl, req, frames, row_pitch, hr, residuals, pupils_out);
+        sl.ticket = t;
+        ctx->next_ticket = t + 1;
+        if (ticket) *ticket = t;
     });
+}
+
+int fpmgpu_wait(fpmgpu_context* ctx, long long ticket, int* lag_used) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (ticket < 0 || ticket >= ctx->next_ticket) throw DataError("unknown reconstruction ticket");
+        HostSlot& sl = slot_for(ctx, ticket);
+        if (sl.ticket == ticket) wait_slot(sl);  // else it completed earlier (its slot was reused)
+        if (lag_used) *lag_used = sl.lag;
+    });
+}
+
+int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames,
+                             int64_t row_pitch, float* hr, double* residuals, float* pupils_out, int* lag_used) {
+    long long t = -1;
+    const int rc = fpmgpu_reconstruct_tiles_async(ctx, req, frames, row_pitch, hr, residuals, pupils_out, &t);
+    if (rc != FPMGPU_OK) return rc;
+    return fpmgpu_wait(ctx, t, lag_used);
 }
 
 struct fpmgpu_online {
@@ -1031,6 +1088,7 @@ struct fpmgpu_online {
     std::unique_ptr<fpmgpu_plan> plan;
     DevBuf<uint16_t> frames;
     DevBuf<double> resid;
+    DevBuf<float2> hr;
     int64_t pitch = 0;
     cudaStream_t copy = nullptr, comp = nullptr;
     std::vector<cudaEvent_t> arrived;  // per frame: its H2D copy is complete
@@ -1116,7 +1174,7 @@ int fpmgpu_online_finish(fpmgpu_online* on, float* hr, double* residuals, float*
         if (on->next < p.L) throw DataError("missing frame for a sequence LED");
         if (r.iters > 1) plan_loop(p, on->frames.p, on->pitch, on->resid.p, p.L, r.iters * p.L, true, on->comp);
         const size_t hr_n = size_t(p.T) * p.N * p.N, pup_n = size_t(p.T) * p.n * p.n;
-        float2* hr_d = hr ? on->ctx->hr.ensure(hr_n) : nullptr;
+        float2* hr_d = hr ? on->hr.ensure(hr_n) : nullptr;
         plan_epilogue(p, reinterpret_cast<float*>(hr_d), nullptr, on->comp);
         if (hr) ck(cudaMemcpyAsync(hr, hr_d, hr_n * sizeof(float2), cudaMemcpyDeviceToHost, on->comp), "hr D2H");
         if (residuals)

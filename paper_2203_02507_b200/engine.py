@@ -426,6 +426,37 @@ def reconstruct_request(req: Request, frames: FrameSet, engine: Engine | None = 
     return hr, res, pup, lag.value
 
 
+class PendingReconstruction:
+    """An in-flight fpmgpu_reconstruct_tiles_async request; wait() returns what
+    reconstruct_request returns. Its buffers stay referenced until then."""
+
+    def __init__(self, eng, ticket, keep, out):
+        self._eng, self._ticket, self._keep, self._out = eng, ticket, keep, out
+
+    def wait(self):
+        lag = C.c_int()
+        check(lib().fpmgpu_wait(self._eng.handle, C.c_longlong(self._ticket), C.byref(lag)))
+        self._keep = None
+        hr, res, pup = self._out
+        return hr, res, pup, lag.value
+
+
+def reconstruct_request_async(req: Request, frames: FrameSet, engine: Engine | None = None) -> PendingReconstruction:
+    """fpmgpu_reconstruct_tiles_async: the request's LR upload may overlap the
+    previous request's reconstruction (two in flight per engine)."""
+    eng = engine or default_engine()
+    r, keep = req.c()
+    T, n, N = r.num_tiles, req.cfg.tile_size, req.cfg.hr_size()
+    imgs = np.ascontiguousarray(frames.images, np.uint16)
+    hr = np.zeros((T, N, N), np.complex64)
+    res = np.zeros((T, req.iters), np.float64)
+    pup = np.zeros((T, n, n), np.complex64)
+    t = C.c_longlong()
+    check(lib().fpmgpu_reconstruct_tiles_async(eng.handle, C.byref(r), imgs.ctypes.data, imgs.shape[2],
+                                               hr.ctypes.data, res.ctypes.data, pup.ctypes.data, C.byref(t)))
+    return PendingReconstruction(eng, t.value, (r, keep, imgs), (hr, res, pup))
+
+
 def reconstruct_tile(frames: FrameSet, tile: TileSpec, cfg: OpticalConfig, iters: int, seq, fft_threads: int = 1,
                      mode: str = "gs", alpha: float = 1.0, beta: float = 1.0,
                      engine: Engine | None = None) -> ReconResult:

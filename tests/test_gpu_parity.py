@@ -339,3 +339,18 @@ def test_cluster_kernel_n64_matches_oracle(orc, eng, monkeypatch, cl):
     amp, ph = amp_phase_rel(got.hr, ref.hr)
     assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
     assert np.allclose(got.metrics.pass_mean_residual, ref.residuals, rtol=1e-3)
+
+
+def test_async_requests_equal_sync(eng):
+    """fpmgpu_reconstruct_tiles_async: three requests in flight back to back (the
+    third waits for the first slot) give the synchronous call's bits."""
+    cfg = gpu_cfg(led_scan_rows=5, led_scan_cols=5, tile_overlap=8)
+    sets = [dataset(cfg, fov=120, seed=50 + k)[0] for k in range(3)]
+    specs = fpm.partition_tiles(120, 120, cfg)
+    seq = fpm.led_sequence("spiral", cfg)
+    reqs = [fpm.make_request(fs, cfg, seq, specs, 2, mode="epry") for fs in sets]
+    sync = [fpm.reconstruct_request(r, fs, eng) for r, fs in zip(reqs, sets)]
+    pend = [fpm.reconstruct_request_async(r, fs, eng) for r, fs in zip(reqs, sets)]
+    for p, ref in zip(pend, sync):
+        hr, res, pup, _ = p.wait()
+        assert np.array_equal(hr, ref[0]) and np.array_equal(res, ref[1]) and np.array_equal(pup, ref[2])
