@@ -29,6 +29,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef FPM_CL_PF8
+#define FPM_CL_PF8 0  // 1: row prefetch for n = 256 too (more registers per thread)
+#endif
+
 namespace fpmk {
 
 size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
@@ -60,7 +64,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     constexpr int SW = NLR / CL;  // columns per CTA
     constexpr int RS = SW + 1;    // slab row stride (float2): column reads conflict-free
     constexpr int NT = NW * 32;
-    constexpr bool PF = M <= 4;  // register room to keep the next row's disk loads in flight
+    constexpr bool PF = M <= 4 || FPM_CL_PF8;  // register room to keep the next row's disk loads in flight
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = int(cluster.block_rank());
     const int tile = blockIdx.x / CL;
