@@ -517,6 +517,9 @@ bool same_request(const HostSlot& c, const fpmgpu_recon_request& r, std::vector<
     ki.insert(ki.end(), r.tile_xy, r.tile_xy + 2 * size_t(r.num_tiles));
     ki.insert(ki.end(), r.offsets, r.offsets + 2 * size_t(r.num_tiles) * r.num_leds);
     ki.insert(ki.end(), r.seq_frame, r.seq_frame + r.num_leds);
+    // kernel-selection overrides change the plans too
+    const char* cl_env = std::getenv("FPM_B200_CLUSTER");
+    ki.insert(ki.end(), {box_forced() ? 1 : 0, cl_env ? std::atoi(cl_env) : -1});
     kd.push_back(r.alpha);
     kd.push_back(r.beta);
     if (r.tile_defocus_um) kd.insert(kd.end(), r.tile_defocus_um, r.tile_defocus_um + r.num_tiles);
