@@ -1,6 +1,9 @@
 // K2/K3 line FFTs (init_canvas, canvas_to_field) and build_pupils.
+#include <cstdlib>
+
 #include "fft_device.cuh"
 #include "kernels.cuh"
+#include "warp_fft.cuh"
 
 namespace fpmk {
 
@@ -123,6 +126,92 @@ __global__ void __launch_bounds__(256) lines_fft(const LinesArgs a) {
     }
 }
 
+// N = 256 lines with one warp per line: the block stages LPB lines in shared
+// memory exactly as lines_fft does (coalesced global traffic), then each warp
+// runs a register/shuffle 256-point FFT (WarpFFT<8>, F1: natural order in,
+// natural order out through the padded layout) instead of four Stockham
+// passes through shared memory. Inverse transforms run as conj(FFT(conj x)).
+// Padded line layout: element i at i + i / 32 (conflict-free for both the
+// lane-strided reads and the digit-reversed writes of F1).
+template <int WHICH>
+__global__ void __launch_bounds__(512) lines_fft_w256(const LinesArgs a) {
+    constexpr int NL = 256, LPB = 16, M = 8, LS = NL + NL / 32;
+    constexpr bool INV = WHICH >= 2;
+    constexpr bool COLS = (WHICH & 1) == 1;
+    __shared__ float2 s[LPB * LS];
+    const int tile = blockIdx.y;
+    const int l0 = blockIdx.x * LPB;
+    const size_t base = size_t(tile) * NL * NL;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    auto pad = [](int i) { return i + (i >> 5); };
+
+    for (int idx = threadIdx.x; idx < LPB * NL; idx += blockDim.x) {
+        int line, e;
+        if (COLS) {
+            e = idx / LPB;
+            line = idx - e * LPB;
+        } else {
+            line = idx / NL;
+            e = idx - line * NL;
+        }
+        float2 x;
+        if (WHICH == 0) {
+            // upsample_bilinear (field.cpp:89-112) of the seed crop's sqrt, pixel-centre mapped
+            const int i = l0 + line, j = e, n = a.n;
+            const float fy = (i + 0.5f) / a.up - 0.5f, fx = (j + 0.5f) / a.up - 0.5f;
+            int ya = int(floorf(fy)), xa = int(floorf(fx));
+            const float wy = fy - ya, wx = fx - xa;
+            const int yb = min(ya + 1, n - 1), xb = min(xa + 1, n - 1);
+            ya = max(ya, 0);
+            xa = max(xa, 0);
+            const int2 txy = a.tile_xy[tile];
+            const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
+            const float v00 = sqrtf(float(f[size_t(ya) * a.pitch + xa]));
+            const float v01 = sqrtf(float(f[size_t(ya) * a.pitch + xb]));
+            const float v10 = sqrtf(float(f[size_t(yb) * a.pitch + xa]));
+            const float v11 = sqrtf(float(f[size_t(yb) * a.pitch + xb]));
+            const float val = (1.f - wy) * ((1.f - wx) * v00 + wx * v01) + wy * ((1.f - wx) * v10 + wx * v11);
+            x = make_float2(((i + j) & 1) ? -val : val, 0.f);
+        } else if (COLS) {
+            x = a.src[base + size_t(e) * NL + l0 + line];
+        } else {
+            const int i = l0 + line;
+            x = a.src[base + size_t(i) * NL + e];
+            if (WHICH == 2 && ((i + e) & 1)) x = cneg(x);
+        }
+        if (INV) x.y = -x.y;
+        s[line * LS + pad(e)] = x;
+    }
+    __syncthreads();
+    {
+        WarpFFT<M> F;
+        F.init_table(l, NL, a.tw);
+        float2* ln = s + w * LS;
+        float2 x[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) x[m] = ln[pad(l + 32 * m)];
+        F.f1(x);  // all lanes have read before the shuffles of f1 complete
+#pragma unroll
+        for (int k0 = 0; k0 < M; ++k0) ln[pad(k0 + M * brev5(l))] = x[k0];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < LPB * NL; idx += blockDim.x) {
+        if (COLS) {
+            const int e = idx / LPB, line = idx - e * LPB;
+            const int i = e, j = l0 + line;
+            float2 x = s[line * LS + pad(e)];
+            if (INV) x.y = -x.y;
+            const float sc = ((i + j) & 1) ? -a.scale : a.scale;
+            a.dst[base + size_t(i) * NL + j] = cscale(x, sc);
+        } else {
+            const int line = idx / NL, e = idx - line * NL;
+            float2 x = s[line * LS + pad(e)];
+            if (INV) x.y = -x.y;
+            a.dst[base + size_t(l0 + line) * NL + e] = x;
+        }
+    }
+}
+
 template <int NL, int LPB, int WHICH>
 cudaError_t launch_lines_t(const LinesArgs& a, int T, cudaStream_t s) {
     const size_t smem = size_t(2) * LPB * NL * sizeof(float2);
@@ -168,9 +257,26 @@ __global__ void build_pupils_kernel(float2* pupils, const uint8_t* support, cons
     }
 }
 
+// FPM_B200_LINES_STOCKHAM=1 keeps N = 256 on the shared-memory Stockham kernel (cross-checks)
+bool lines_stockham_forced() {
+    const char* e = std::getenv("FPM_B200_LINES_STOCKHAM");
+    return e && e[0] == '1';
+}
+
 }  // namespace
 
 cudaError_t launch_lines(int which, int N, const LinesArgs& a, int T, cudaStream_t s) {
+    if (N == 256 && !lines_stockham_forced()) {
+        const dim3 grid(256 / 16, T);
+        switch (which) {
+            case 0: lines_fft_w256<0><<<grid, 512, 0, s>>>(a); break;
+            case 1: lines_fft_w256<1><<<grid, 512, 0, s>>>(a); break;
+            case 2: lines_fft_w256<2><<<grid, 512, 0, s>>>(a); break;
+            case 3: lines_fft_w256<3><<<grid, 512, 0, s>>>(a); break;
+            default: return cudaErrorInvalidValue;
+        }
+        return cudaGetLastError();
+    }
     switch (N) {
         case 256: return launch_lines_n<256, 16>(which, a, T, s);
         case 512: return launch_lines_n<512, 8>(which, a, T, s);

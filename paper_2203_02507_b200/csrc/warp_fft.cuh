@@ -60,6 +60,22 @@ struct WarpFFT {
             tw[k0] = make_float4(float(c), float(s), -float(s), float(c));
         }
     }
+    // the same constants from a table tab[m] = W_n^m (m in [0, n)) in global memory
+    __device__ void init_table(int l, int n, const float2* __restrict__ tab) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const int h = 1 << k;
+            const bool up = (l & h) != 0;
+            const float2 w = up ? __ldg(tab + (l & (h - 1)) * (n / (2 * h))) : make_float2(1.f, 0.f);
+            cw[k] = make_float4(w.x, w.y, -w.y, w.x);
+            sgk[k] = up ? -1.f : 1.f;
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < M; ++k0) {
+            const float2 w = __ldg(tab + (l * k0) % n);
+            tw[k0] = make_float4(w.x, w.y, -w.y, w.x);
+        }
+    }
     static __device__ __forceinline__ float2 mul(float2 v, const float4& w) {
         return cmul_sw(v, make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
