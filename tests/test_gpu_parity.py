@@ -354,3 +354,64 @@ def test_async_requests_equal_sync(eng):
     for p, ref in zip(pend, sync):
         hr, res, pup, _ = p.wait()
         assert np.array_equal(hr, ref[0]) and np.array_equal(res, ref[1]) and np.array_equal(pup, ref[2])
+
+
+def _rect_dataset(cfg, h, w, seed, order="spiral", defocus=0.0, noise=None):
+    from tests.helpers import orc
+    oc = orc_cfg(cfg)
+    size = max(h, w) * cfg.upsample
+    obj = orc.synth_object("composite", max(size, 256), seed)[: h * cfg.upsample, : w * cfg.upsample]
+    seq = orc.led_sequence(order, oc)
+    fs = orc.simulate_dataset(obj, seq, oc, noise=noise, defocus_um=defocus)
+    return fpm.FrameSet(fs.images, list(fs.leds), fs.timestamps), fs, seq
+
+
+def test_rectangular_fov_with_clamped_tiles(orc):
+    """Non-square FOV (120 x 184 LR px, overlap 8): clamped last tiles on both
+    axes, raster order, EPRY with per-tile defocus; tiles and Eq. (1) mosaic
+    against the oracle."""
+    cfg = gpu_cfg(led_scan_rows=5, led_scan_cols=5, tile_overlap=8)
+    fs, ofs, seq = _rect_dataset(cfg, 120, 184, seed=60, order="raster", defocus=4.0)
+    specs = fpm.partition_tiles(184, 120, cfg)
+    assert len(specs) == 2 * 4  # x: 0, 56, 112, 120 (clamped); y: 0, 56
+    dz = np.linspace(-6, 6, len(specs))
+    opt = fpm.RunOptions(iters=3, mode="epry", tile_defocus_um=list(dz))
+    got = fpm.run_offline(fs, cfg, seq, opt)
+    ref = orc.run_offline(ofs, orc_cfg(cfg), seq, 3, mode="epry", tile_defocus=dz)
+    assert got.stitched.shape == ref.stitched.shape == (480, 736)
+    for i in range(len(specs)):
+        amp, ph = amp_phase_rel(got.tiles[i], ref.tiles[i])
+        assert amp < FINAL_TOL and ph < FINAL_TOL, (i, amp, ph)
+    amp, ph = amp_phase_rel(got.stitched, ref.stitched)
+    assert amp < FINAL_TOL and ph < FINAL_TOL, (amp, ph)
+
+
+def test_noisy_stack_and_upsample_8(orc):
+    """Photon-noise frames (the reference's Poisson model) and a finer HR grid
+    (upsample 8: N = 512 canvases for 64-px tiles) through the lattice kernel."""
+    cfg = gpu_cfg(led_scan_rows=5, led_scan_cols=5, tile_overlap=0, upsample=8)
+    fs, ofs, seq = _rect_dataset(cfg, 64, 64, seed=61, noise=(2000.0, 7))
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    got = fpm.reconstruct_tile(fs, t, cfg, 2, seq, mode="gs")
+    ref = orc.reconstruct_tile(ofs, orc_cfg(cfg), 2, seq, mode="gs")
+    assert got.hr.shape == (512, 512)
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
+    assert np.allclose(got.metrics.pass_mean_residual, ref.residuals, rtol=1e-3)
+
+
+def test_seed_frame_missing_uses_brightest(orc, capsys):
+    """No on-axis frame: init_canvas seeds from the brightest frame with the
+    reference's warning (recon.cpp:64-75); results still match the oracle."""
+    cfg = gpu_cfg(led_scan_rows=3, led_scan_cols=3)
+    fs, ofs, seq, _ = dataset(cfg, seed=62)
+    keep = [k for k, led in enumerate(fs.leds) if tuple(led) != cfg.center_led]
+    fs2 = fpm.FrameSet(fs.images[keep], [fs.leds[k] for k in keep])
+    ofs2 = orc.FrameStack(fs.images[keep], [fs.leds[k] for k in keep])
+    seq2 = [s for s in seq if tuple(s) != cfg.center_led]
+    t = fpm.partition_tiles(64, 64, cfg)[0]
+    got = fpm.reconstruct_tile(fs2, t, cfg, 2, seq2)
+    assert "brightest frame" in capsys.readouterr().err
+    ref = orc.reconstruct_tile(ofs2, orc_cfg(cfg), 2, seq2)
+    amp, ph = amp_phase_rel(got.hr, ref.hr)
+    assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
