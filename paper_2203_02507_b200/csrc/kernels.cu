@@ -89,6 +89,14 @@ __device__ __forceinline__ float2 shfl_pair(float2 x) {
     return make_float2(__shfl_xor_sync(kFull, x.x, 1), __shfl_xor_sync(kFull, x.y, 1));
 }
 
+// v * (-i) on the odd lane of a pair, v on the even one (the pair twiddle W8^2):
+// selects and a sign-bit flip on the ALU pipe instead of a two-instruction
+// packed multiply on the FMA pipe
+__device__ __forceinline__ float2 mul_mi_odd(float2 v, int h) {
+    const float nx = __int_as_float(__float_as_int(v.x) ^ int(0x80000000u));
+    return h ? make_float2(v.y, nx) : v;
+}
+
 // transpose swizzle of destination row p': XOR on slot bits 1 and 3
 __device__ __forceinline__ int tswz(int pp) {
     return ((pp & 1) << 1) | ((((pp >> 1) ^ (pp >> 2)) & 1) << 3);
@@ -122,7 +130,8 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
 #pragma unroll
-        for (int m = 1; m < 4; ++m) v[a][m] = cmul_sw(v[a][m], tw[m], twsw[m]);  // O' = W8^m O
+        for (int m = 1; m < 4; ++m)  // O' = W8^m O (m = 2: -i, a swap and a sign off the FMA pipe)
+            v[a][m] = m == 2 ? mul_mi_odd(v[a][m], h) : cmul_sw(v[a][m], tw[m], twsw[m]);
 #pragma unroll
         for (int m = 0; m < 4; ++m) v[a][m] = cfma(sg, v[a][m], shfl_pair(v[a][m]));  // E + O' | E - O'
     }
@@ -173,7 +182,8 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
 #pragma unroll
         for (int i = 0; i < 4; ++i) v[a][i] = cfma(sg, v[a][i], shfl_pair(v[a][i]));  // y_i + y_(i+4) | y_i - y_(i+4)
 #pragma unroll
-        for (int i = 1; i < 4; ++i) v[a][i] = cmul_sw(v[a][i], tw[i], twsw[i]);
+        for (int i = 1; i < 4; ++i)
+            v[a][i] = i == 2 ? mul_mi_odd(v[a][i], h) : cmul_sw(v[a][i], tw[i], twsw[i]);
         if (skip_rows)  // the scatter reads columns j in {1, 2} of these rows only
             dft4_o12<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
         else
