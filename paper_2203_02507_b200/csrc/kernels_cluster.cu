@@ -55,6 +55,9 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
                  "l"(gsrc)
                  : "memory");
 }
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -159,6 +162,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
         const int e_next = next_entry(e);
         const short2 o = O_s[pos];
         float2* cv = canvas + size_t(o.x) * NC + o.y;
+        // box rows are owned by canvas row (o.x + i) mod CL: a CTA reads in phase A only
+        // canvas rows it wrote itself in earlier phases C, so consecutive updates need no
+        // cross-CTA ordering of canvas memory (the disk moves with the LED)
+        const int rfirst = b0 + ((rank - (int(o.x) + b0) % CL) % CL + CL) % CL;
 
         // ---- A: IFFT of this CTA's box rows, outputs to the column owners
         // the disk loads of a warp's next row are issued before the current row's FFT
@@ -175,7 +182,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
                 Pa[k0] = on ? pupil[ii * NLR + c] : make_float2(0.f, 0.f);
             }
         };
-        const int i0 = b0 + rank + CL * w;
+        const int i0 = rfirst + CL * w;
         if (PF && i0 < b0 + B) load_row(i0);
         for (int i = i0; i < b0 + B; i += CL * NW) {
             float2 x[M];
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
         const float inv_omax = upd[0], inv_pmax = upd[1];
 
         // ---- C: FFT of this CTA's box rows (fetched from the column slabs), scatter
-        for (int i = b0 + rank + CL * w; i < b0 + B; i += CL * NW) {
+        for (int i = rfirst + CL * w; i < b0 + B; i += CL * NW) {
             // the scatter's disk operands are loaded first, their latency under the FFT
             const short2 run = SR[i];
             float2 Pc[PF ? M : 1], Oc[PF ? M : 1];
@@ -351,7 +358,13 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
                 }
             }
         }
-        cluster.sync();  // slabs reusable; canvas and pupil writes visible to the whole cluster
+        // slabs reusable. Only a pupil step (bright-field EPRY) leaves writes another CTA
+        // reads next (pupil rows follow the moving box rows): then release; else a relaxed
+        // arrive skips the fence that would wait for this phase's canvas stores
+        if (MODE == kModeEPRY && inv_omax > 0.f)
+            cluster.sync();
+        else
+            cluster_sync_relaxed();
         e = e_next;
     }
     if (rank == 0) store_residuals(args, tile, stage_sum, G == 1);
