@@ -400,7 +400,7 @@ cudaError_t launch_cluster_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStr
 int cluster_warps(int n, int cl) { return (n == 64 || cl == 16) ? 4 : (n == 256 && cl == 2) ? 16 : 8; }
 
 bool cluster_supported(int n, int N, int cl) {
-    if (n == 64) return N == 256 && (cl == 4 || cl == 8);
+    if (n == 64) return N == 256 && (cl == 4 || cl == 8 || cl == 16);
     if (n == 128) return N == 512 && (cl == 2 || cl == 4 || cl == 8 || cl == 16);
     if (n == 256) return N == 1024 && (cl == 2 || cl == 4 || cl == 8);
     return false;
@@ -414,6 +414,7 @@ cudaError_t launch_loop_cluster(int n, int mode, int cl, const LoopArgs& a, cons
                                : launch_cluster_t<NN, kModeEPRY, NCC, CLL, NWW>(a, b, T, s);
     FPM_CL_CASE(64, 256, 4, 4)
     FPM_CL_CASE(64, 256, 8, 4)
+    FPM_CL_CASE(64, 256, 16, 4)
     FPM_CL_CASE(128, 512, 2, 8)
     FPM_CL_CASE(128, 512, 4, 8)
     FPM_CL_CASE(128, 512, 8, 8)
