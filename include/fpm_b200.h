@@ -130,7 +130,8 @@ int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* re
  * LR upload runs under request k's reconstruction (two staging slots per
  * context; a third submit first waits for the oldest). The host buffers of a
  * request must stay valid and untouched until fpmgpu_wait(ticket) returns;
- * use pinned memory for the copies to be asynchronous. */
+ * use pinned memory for the copies to be asynchronous. A request older than the
+ * two slots completed when its slot was reused; waiting on it returns at once. */
 int fpmgpu_reconstruct_tiles_async(fpmgpu_context* ctx, const fpmgpu_recon_request* req,
                                    const uint16_t* frames, int64_t row_pitch, float* hr,
                                    double* residuals, float* pupils_out, long long* ticket);

@@ -215,6 +215,7 @@ struct fpmgpu_context {
     // host path: two slots, so request k + 1's upload overlaps request k's reconstruction
     HostSlot slots[2];
     long long next_ticket = 0;
+    int lag_of[2] = {0, 0};  // lag of the request last submitted on each slot
 
     const float2* twiddle_table(int N) {
         DevBuf<float2>* b = N == 256 ? &tw256 : N == 512 ? &tw512 : N == 1024 ? &tw1024 : nullptr;
@@ -1063,6 +1064,7 @@ int fpmgpu_reconstruct_tiles_async(fpmgpu_context* ctx, const fpmgpu_recon_reque
         wait_slot(sl);  // its buffers and plans are free once request t - 2 is done
         submit(ctx, sl, req, frames, row_pitch, hr, residuals, pupils_out);
         sl.ticket = t;
+        ctx->lag_of[t & 1] = sl.lag;
         ctx->next_ticket = t + 1;
         if (ticket) *ticket = t;
     });
@@ -1072,9 +1074,10 @@ int fpmgpu_wait(fpmgpu_context* ctx, long long ticket, int* lag_used) {
     return guarded([&] {
         ck(cudaSetDevice(ctx->device), "cudaSetDevice");
         if (ticket < 0 || ticket >= ctx->next_ticket) throw DataError("unknown reconstruction ticket");
+        // a ticket older than the two slots completed when its slot was reused
         HostSlot& sl = slot_for(ctx, ticket);
-        if (sl.ticket == ticket) wait_slot(sl);  // else it completed earlier (its slot was reused)
-        if (lag_used) *lag_used = sl.lag;
+        if (sl.ticket == ticket) wait_slot(sl);
+        if (lag_used) *lag_used = ctx->lag_of[ticket & 1];
     });
 }
 
