@@ -917,9 +917,8 @@ namespace {
 // so band b's LR rows can cross PCIe while band b-1 already reconstructs and
 // band b-2's HR tiles travel back. FPM_B200_BANDS overrides the count (1 = off).
 // The pipelined schedule picks ONE lag for the whole batch, so it stays unbanded.
-std::vector<int> host_bands(const fpmgpu_recon_request& r) {
+std::vector<int> host_bands(const fpmgpu_recon_request& r, int want) {
     const int T = r.num_tiles;
-    int want = 8;
     if (const char* e = std::getenv("FPM_B200_BANDS")) want = std::max(1, std::atoi(e));
     std::vector<int> row_start;  // tile indices where a new tile row begins
     for (int t = 0; t < T; ++t)
@@ -948,12 +947,12 @@ void wait_slot(HostSlot& sl) {
 
 // Enqueue one host-buffer reconstruction on slot `sl` (returns before it completes).
 void submit(fpmgpu_context* ctx, HostSlot& sl, const fpmgpu_recon_request* req, const uint16_t* frames,
-            int64_t row_pitch, float* hr, double* residuals, float* pupils_out) {
+            int64_t row_pitch, float* hr, double* residuals, float* pupils_out, int bands) {
     cudaStream_t s = ctx->stream;
     std::vector<int> ki;
     std::vector<double> kd;
     std::vector<float> kf;
-    const std::vector<int> t0 = host_bands(*req);
+    const std::vector<int> t0 = host_bands(*req, bands);
     const int B = int(t0.size()) - 1;
     const bool hit = same_request(sl, *req, ki, kd, kf) && sl.band_t0 == t0;
     if (!hit) {
@@ -1054,20 +1053,33 @@ HostSlot& slot_for(fpmgpu_context* ctx, long long ticket) { return ctx->slots[ti
 
 }  // namespace
 
-int fpmgpu_reconstruct_tiles_async(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames,
-                                   int64_t row_pitch, float* hr, double* residuals, float* pupils_out,
-                                   long long* ticket) {
+namespace {
+
+// Bands per request (measured on config 3): a lone call hides its upload best
+// with 8 bands (54 ms vs 56 with 4); back-to-back calls already overlap one
+// request's upload with the previous reconstruction, and 4 bands keep the
+// launches larger (38.7 ms per request vs 41.8 with 8).
+int submit_async(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames, int64_t row_pitch,
+                 float* hr, double* residuals, float* pupils_out, long long* ticket, int bands) {
     return guarded([&] {
         ck(cudaSetDevice(ctx->device), "cudaSetDevice");
         const long long t = ctx->next_ticket;
         HostSlot& sl = slot_for(ctx, t);
         wait_slot(sl);  // its buffers and plans are free once request t - 2 is done
-        submit(ctx, sl, req, frames, row_pitch, hr, residuals, pupils_out);
+        submit(ctx, sl, req, frames, row_pitch, hr, residuals, pupils_out, bands);
         sl.ticket = t;
         ctx->lag_of[t & 1] = sl.lag;
         ctx->next_ticket = t + 1;
         if (ticket) *ticket = t;
     });
+}
+
+}  // namespace
+
+int fpmgpu_reconstruct_tiles_async(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames,
+                                   int64_t row_pitch, float* hr, double* residuals, float* pupils_out,
+                                   long long* ticket) {
+    return submit_async(ctx, req, frames, row_pitch, hr, residuals, pupils_out, ticket, 4);
 }
 
 int fpmgpu_wait(fpmgpu_context* ctx, long long ticket, int* lag_used) {
@@ -1084,7 +1096,7 @@ int fpmgpu_wait(fpmgpu_context* ctx, long long ticket, int* lag_used) {
 int fpmgpu_reconstruct_tiles(fpmgpu_context* ctx, const fpmgpu_recon_request* req, const uint16_t* frames,
                              int64_t row_pitch, float* hr, double* residuals, float* pupils_out, int* lag_used) {
     long long t = -1;
-    const int rc = fpmgpu_reconstruct_tiles_async(ctx, req, frames, row_pitch, hr, residuals, pupils_out, &t);
+    const int rc = submit_async(ctx, req, frames, row_pitch, hr, residuals, pupils_out, &t, 8);
     if (rc != FPMGPU_OK) return rc;
     return fpmgpu_wait(ctx, t, lag_used);
 }
