@@ -37,12 +37,13 @@ namespace fpmk {
 
 size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
     const size_t sw = size_t(n / cl);
-    size_t b = size_t(box) * (sw + 1) * sizeof(float2);  // column slab of the box rows
+    const size_t nbuf = n <= 128 ? 2 : 1;                  // double-buffered slabs (small n)
+    size_t b = nbuf * size_t(box) * (sw + 1) * sizeof(float2);  // column slab(s) of the box rows
     b += sw * size_t(n) * sizeof(uint16_t);               // measurement slab
     b += size_t(n) * sizeof(short2);                      // support run per row
     b = (b + 15) & ~size_t(15);
     b += size_t(iters) * sizeof(double);
-    b += size_t(nw) * 4 * sizeof(float) + 4 * sizeof(float);
+    b += nbuf * size_t(nw) * 4 * sizeof(float) + 4 * sizeof(float);
     b += size_t(L) * (sizeof(short2) + sizeof(int) + 1) + 16;
     return b;
 }
@@ -68,6 +69,9 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     constexpr int RS = SW + 1;    // slab row stride (float2): column reads conflict-free
     constexpr int NT = NW * 32;
     constexpr bool PF = M <= 4 || FPM_CL_PF8;  // register room to keep the next row's disk loads in flight
+    // DB: two slab / reduction buffers used alternately, so an update's phase A never
+    // overwrites what the previous update's phase C still reads: no end-of-update barrier
+    constexpr bool DB = NLR <= 128;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = int(cluster.block_rank());
     const int tile = blockIdx.x / CL;
@@ -75,8 +79,13 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     const int L = args.L, B = bx.box, b0 = bx.b0;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* sp = smem_raw;
-    float2* S = reinterpret_cast<float2*>(sp);
+    float2* S0 = reinterpret_cast<float2*>(sp);
     sp += size_t(B) * RS * sizeof(float2);
+    float2* S1 = S0;
+    if (DB) {
+        S1 = reinterpret_cast<float2*>(sp);
+        sp += size_t(B) * RS * sizeof(float2);
+    }
     uint16_t* I_s = reinterpret_cast<uint16_t*>(sp);  // [row][column ^ isw(row)]
     sp += size_t(SW) * NLR * sizeof(uint16_t);
     short2* SR = reinterpret_cast<short2*>(sp);  // support run [x, y) of each row
@@ -84,8 +93,13 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     sp = smem_raw + ((sp - smem_raw + 15) & ~15);
     double* stage_sum = reinterpret_cast<double*>(sp);
     sp += size_t(args.iters) * sizeof(double);
-    float* wred = reinterpret_cast<float*>(sp);  // [warp][4]: num, den, omax, pmax
+    float* wred0 = reinterpret_cast<float*>(sp);  // [warp][4]: num, den, omax, pmax
     sp += NW * 4 * sizeof(float);
+    float* wred1 = wred0;
+    if (DB) {
+        wred1 = reinterpret_cast<float*>(sp);
+        sp += NW * 4 * sizeof(float);
+    }
     float* upd = reinterpret_cast<float*>(sp);  // inv_omax, inv_pmax of the current update
     sp += 4 * sizeof(float);
     short2* O_s = reinterpret_cast<short2*>(sp);
@@ -156,9 +170,12 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
         entry_at(e, it0, pos0);
         stage(pos0);
     }
+    int par = 0;
     for (; e >= 0;) {
         int it, pos;
         entry_at(e, it, pos);
+        float2* const S = par ? S1 : S0;
+        float* const wred = par ? wred1 : wred0;
         const int e_next = next_entry(e);
         const short2 o = O_s[pos];
         float2* cv = canvas + size_t(o.x) * NC + o.y;
@@ -361,12 +378,16 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
         // slabs reusable. Only a pupil step (bright-field EPRY) leaves writes another CTA
         // reads next (pupil rows follow the moving box rows): then release; else a relaxed
         // arrive skips the fence that would wait for this phase's canvas stores
-        if (MODE == kModeEPRY && inv_omax > 0.f)
+        if (MODE == kModeEPRY && inv_omax > 0.f) {
             cluster.sync();
-        else
-            cluster_sync_relaxed();
+        } else {
+            __syncthreads();  // a canvas row's next reader may be another warp of this CTA
+            if (!DB) cluster_sync_relaxed();  // single slab buffer: phase C reads done
+        }
+        par ^= DB ? 1 : 0;
         e = e_next;
     }
+    if (DB) cluster.sync();  // no CTA leaves while another still reads its slab
     if (rank == 0) store_residuals(args, tile, stage_sum, G == 1);
 }
 
