@@ -102,11 +102,11 @@ __device__ __forceinline__ int tswz(int pp) {
     return ((pp & 1) << 1) | ((((pp >> 1) ^ (pp >> 2)) & 1) << 3);
 }
 
-// One forward transform body serves both directions (IFFT(x) = conj(FFT(conj x)),
-// the conjugations folded into gather and modulus), so the update loop carries a
-// single FFT copy: half the instruction footprint of two specialised bodies.
-// The prunings become warp-uniform branches: skip_cols drops the zero columns of
-// the disk-limited input (IFFT), skip_rows the rows the scatter never reads (FFT).
+// One forward transform serves both directions (IFFT(x) = conj(FFT(conj x)), the
+// conjugations folded into gather and modulus). The update loop instantiates it
+// once per pass (FPM_PASS_UNROLL, measured 2% faster than one rolled body), so
+// the prunings resolve at compile time: skip_cols drops the zero columns of the
+// disk-limited input (IFFT), skip_rows the rows the scatter never reads (FFT).
 __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, const float4* W4_s, int p, int h,
                                                 float sg, const float2 (&tw)[4], const float2 (&twsw)[4], int g,
                                                 bool skip_cols, bool skip_rows) {
