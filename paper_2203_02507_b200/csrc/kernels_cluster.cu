@@ -69,6 +69,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     constexpr int RS = SW + 1;    // slab row stride (float2): column reads conflict-free
     constexpr int NT = NW * 32;
     constexpr bool PF = M <= 4 || FPM_CL_PF8;  // register room to keep the next row's disk loads in flight
+#ifndef FPM_CL_PFC8
+#define FPM_CL_PFC8 0
+#endif
+    constexpr bool PFC = M <= 4 || FPM_CL_PFC8;  // phase C: scatter operands loaded before the FFT
     // DB: two slab / reduction buffers used alternately, so an update's phase A never
     // overwrites what the previous update's phase C still reads: no end-of-update barrier
     constexpr bool DB = NLR <= 128;
@@ -338,8 +342,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
         for (int i = rfirst + CL * w; i < b0 + B; i += CL * NW) {
             // the scatter's disk operands are loaded first, their latency under the FFT
             const short2 run = SR[i];
-            float2 Pc[PF ? M : 1], Oc[PF ? M : 1];
-            if constexpr (PF) {
+            float2 Pc[PFC ? M : 1], Oc[PFC ? M : 1];
+            if constexpr (PFC) {
 #pragma unroll
                 for (int k0 = 0; k0 < M; ++k0) {
                     const int c = k0 + M * brev5(l);
@@ -363,12 +367,12 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
                 float2* dst = cv + size_t(i) * NC + c;
                 float2* pp = pupil + i * NLR + c;
                 float2 P;
-                if constexpr (PF) P = Pc[k0]; else P = *pp;
+                if constexpr (PFC) P = Pc[k0]; else P = *pp;
                 if (MODE == kModeGS) {
                     *dst = cmulc(psi2, P);
                 } else {
                     float2 O;
-                    if constexpr (PF) O = Oc[k0]; else O = *dst;
+                    if constexpr (PFC) O = Oc[k0]; else O = *dst;
                     const float2 d = csub(psi2, cmul(O, P));
                     if (inv_pmax > 0.f) *dst = cadd(O, cscale(cmulc(d, P), inv_pmax));
                     if (inv_omax > 0.f) *pp = cadd(P, cscale(cmulc(d, O), inv_omax));
