@@ -39,9 +39,10 @@ __device__ __forceinline__ void dftM(float2 (&x)[M]) {
 // conj(FFT(conj x)), the conjugations folded into the callers' loads and stores.
 template <int M>
 struct WarpFFT {
-    float4 cw[5];
+    float4 cw[5];  // cw[0] = 1 and cw[1] in {1, -i} are applied without multiplies (stage())
     float sgk[5];
     float4 tw[M];
+    bool mi = false;  // lane of stage h = 2 whose twiddle is -i ((l & 3) == 3)
     __device__ void init(int l, int n) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
@@ -53,6 +54,7 @@ struct WarpFFT {
             cw[k] = make_float4(wc, ws, -ws, wc);
             sgk[k] = up ? -1.f : 1.f;
         }
+        mi = (l & 3) == 3;
 #pragma unroll
         for (int k0 = 0; k0 < M; ++k0) {
             double s, c;
@@ -70,6 +72,7 @@ struct WarpFFT {
             cw[k] = make_float4(w.x, w.y, -w.y, w.x);
             sgk[k] = up ? -1.f : 1.f;
         }
+        mi = (l & 3) == 3;
 #pragma unroll
         for (int k0 = 0; k0 < M; ++k0) {
             const float2 w = __ldg(tab + (l * k0) % n);
@@ -79,27 +82,50 @@ struct WarpFFT {
     static __device__ __forceinline__ float2 mul(float2 v, const float4& w) {
         return cmul_sw(v, make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
+    // lane twiddle of stage k: W_2^0 = 1 (none), W_4^(l mod 2) in {1, -i} (a lane-selected
+    // swap and sign on the ALU pipe), a packed complex multiply from stage 2 on
+    template <int K>
+    __device__ __forceinline__ float2 stage(float2 v) const {
+        if constexpr (K == 0) {
+            return v;
+        } else if constexpr (K == 1) {
+            const float nx = __int_as_float(__float_as_int(v.x) ^ int(0x80000000u));
+            return mi ? make_float2(v.y, nx) : v;
+        } else {
+            return mul(v, cw[K]);
+        }
+    }
     // F1: x[l + 32 m] -> X[k0 + M br5(l)]: register DFT, twiddle, lane DIF
     __device__ __forceinline__ void f1(float2 (&x)[M]) const {
         dftM<false, M>(x);
 #pragma unroll
         for (int k0 = 1; k0 < M; ++k0) x[k0] = mul(x[k0], tw[k0]);
+        dif_stage<4>(x);
+        dif_stage<3>(x);
+        dif_stage<2>(x);
+        dif_stage<1>(x);
+        dif_stage<0>(x);
+    }
+    template <int K>
+    __device__ __forceinline__ void dif_stage(float2 (&x)[M]) const {  // h = 2^K
 #pragma unroll
-        for (int k = 4; k >= 0; --k) {  // h = 16 .. 1
+        for (int k0 = 0; k0 < M; ++k0) x[k0] = stage<K>(cfma(sgk[K], x[k0], shfl_x(x[k0], 1 << K)));
+    }
+    template <int K>
+    __device__ __forceinline__ void dit_stage(float2 (&x)[M]) const {  // h = 2^K
 #pragma unroll
-            for (int k0 = 0; k0 < M; ++k0) x[k0] = mul(cfma(sgk[k], x[k0], shfl_x(x[k0], 1 << k)), cw[k]);
+        for (int k0 = 0; k0 < M; ++k0) {
+            const float2 b = stage<K>(x[k0]);
+            x[k0] = cfma(sgk[K], b, shfl_x(b, 1 << K));
         }
     }
     // F2: x[k0 + M br5(l)] -> X[q + 32 r]: lane DIT, twiddle, register DFT
     __device__ __forceinline__ void f2(float2 (&x)[M]) const {
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {  // h = 1 .. 16
-#pragma unroll
-            for (int k0 = 0; k0 < M; ++k0) {
-                const float2 b = mul(x[k0], cw[k]);
-                x[k0] = cfma(sgk[k], b, shfl_x(b, 1 << k));
-            }
-        }
+        dit_stage<0>(x);
+        dit_stage<1>(x);
+        dit_stage<2>(x);
+        dit_stage<3>(x);
+        dit_stage<4>(x);
 #pragma unroll
         for (int k0 = 1; k0 < M; ++k0) x[k0] = mul(x[k0], tw[k0]);
         dftM<false, M>(x);
