@@ -42,7 +42,7 @@ size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
     b += sw * size_t(n) * sizeof(uint16_t);               // measurement slab
     b += size_t(n) * sizeof(short2);                      // support run per row
     b = (b + 15) & ~size_t(15);
-    b += size_t(iters) * sizeof(double);
+    b += size_t(iters) * sizeof(double) + 2 * sizeof(uint64_t);
     b += nbuf * size_t(nw) * 4 * sizeof(float) + 4 * sizeof(float);
     b += size_t(L) * (sizeof(short2) + sizeof(int) + 1) + 16;
     return b;
@@ -58,6 +58,41 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cluster_sync_relaxed() {
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// asynchronous store of 8 bytes into another CTA's shared memory; completion is
+// counted in bytes on that CTA's mbarrier (no release fence on this side)
+__device__ __forceinline__ void st_async_f2(uint32_t raddr, float2 v, uint32_t rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "f"(v.x), "f"(v.y), "r"(rmbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
@@ -97,6 +132,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     sp = smem_raw + ((sp - smem_raw + 15) & ~15);
     double* stage_sum = reinterpret_cast<double*>(sp);
     sp += size_t(args.iters) * sizeof(double);
+    uint64_t* mbA = reinterpret_cast<uint64_t*>(sp);  // DB: phase-A slab arrivals, one per parity
+    sp += 2 * sizeof(uint64_t);
     float* wred0 = reinterpret_cast<float*>(sp);  // [warp][4]: num, den, omax, pmax
     sp += NW * 4 * sizeof(float);
     float* wred1 = wred0;
@@ -125,6 +162,11 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     WarpFFT<M> F;
     F.init(l, NLR);
     const float inv_n2 = 1.0f / float(NLR * NLR);
+    if (DB && threadIdx.x == 0) {
+        mbar_init1(mbA);
+        mbar_init1(mbA + 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     cluster.sync();  // every CTA of the cluster is resident before any DSMEM access
 
     // schedule entries: sequential slot e = (e / L, e % L); pipelined slots hold two
@@ -175,11 +217,14 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
         stage(pos0);
     }
     int par = 0;
+    uint32_t nupd = 0;  // updates run by this launch (mbarrier phase of buffer `par` = (nupd >> 1) & 1)
     for (; e >= 0;) {
         int it, pos;
         entry_at(e, it, pos);
         float2* const S = par ? S1 : S0;
         float* const wred = par ? wred1 : wred0;
+        // DB: this update's slab arrives by st.async, counted on mbA[par] (B rows x SW columns)
+        if (DB && threadIdx.x == 0) mbar_arm(mbA + par, uint32_t(B) * SW * sizeof(float2));
         const int e_next = next_entry(e);
         const short2 o = O_s[pos];
         float2* cv = canvas + size_t(o.x) * NC + o.y;
@@ -242,7 +287,12 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
 #pragma unroll
             for (int r = 0; r < M; ++r) {
                 const int col = l + 32 * r, owner = col / SW;
-                cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)] = x[r];
+                if constexpr (DB) {
+                    const uint32_t off = uint32_t((size_t(i - b0) * RS + (col - owner * SW)) * sizeof(float2));
+                    st_async_f2(map_rank(smem_addr(S) + off, owner), x[r], map_rank(smem_addr(mbA + par), owner));
+                } else {
+                    cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)] = x[r];
+                }
             }
         }
         if (MODE == kModeEPRY) {
@@ -257,7 +307,12 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
             }
         }
         cp_async_wait_all();  // this thread's part of the measurement slab has landed
-        cluster.sync();
+        if constexpr (DB) {
+            __syncthreads();  // measurement slab and the EPRY partials visible CTA-wide
+            mbar_wait_parity(mbA + par, (nupd >> 1) & 1u);  // every column of every box row landed
+        } else {
+            cluster.sync();
+        }
 
         // ---- B: this CTA's columns: IFFT over the box rows -> modulus -> FFT -> box rows
         float num = 0.f, den = 0.f;
@@ -389,6 +444,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
             if (!DB) cluster_sync_relaxed();  // single slab buffer: phase C reads done
         }
         par ^= DB ? 1 : 0;
+        ++nupd;
         e = e_next;
     }
     if (DB) cluster.sync();  // no CTA leaves while another still reads its slab
