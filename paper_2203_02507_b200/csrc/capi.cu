@@ -56,6 +56,8 @@ int guarded(F&& f) {
 }
 
 void ck(cudaError_t e, const char* what) {
+    if (e == cudaErrorNotSupported)  // the launchers' "no kernel instantiated for this geometry"
+        throw Unsupported(std::string(what) + ": no kernel for this tile / canvas geometry in this build");
     if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
@@ -334,6 +336,7 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
         const bool smem_s = p.n != 256;
         if (p.n == 256 && p.N != 1024) throw Unsupported("n = 256 runs with canvas side 1024 (upsample 4) in this build");
         if (p.n == 128 && p.N != 512 && p.N != 1024) throw Unsupported("n = 128 needs canvas side 512 or 1024");
+        if (p.n == 64 && p.N != 256) throw Unsupported("the box kernel runs n = 64 with canvas side 256 only");
         if (!smem_s) p.scratch.ensure(size_t(p.T) * p.box * (p.n + 1));
     } else {
         lattice_shape(sup, &p.nslots, &p.prune);

@@ -523,7 +523,7 @@ cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorM
     FPM_LOOP_CASE(kModeEPRY, false, kMeasF32, 1, 256)
 #undef FPM_LOOP_N
 #undef FPM_LOOP_CASE
-    return cudaErrorInvalidConfiguration;
+    return cudaErrorNotSupported;  // no instantiation for this geometry
 }
 
 }  // namespace fpmk

@@ -268,7 +268,7 @@ cudaError_t launch_loop_box(int n, int mode, const LoopArgs& a, const BoxArgs& b
     FPM_BOX_CASE(64, kModeGS, 256, true)
     FPM_BOX_CASE(64, kModeEPRY, 256, true)
 #undef FPM_BOX_CASE
-    return cudaErrorInvalidConfiguration;
+    return cudaErrorNotSupported;  // no instantiation for this geometry
 }
 
 }  // namespace fpmk

@@ -504,7 +504,7 @@ cudaError_t launch_loop_cluster(int n, int mode, int cl, const LoopArgs& a, cons
     FPM_CL_CASE(256, 1024, 4, 8)
     FPM_CL_CASE(256, 1024, 8, 8)
 #undef FPM_CL_CASE
-    return cudaErrorInvalidValue;
+    return cudaErrorNotSupported;  // no instantiation for this geometry
 }
 
 }  // namespace fpmk

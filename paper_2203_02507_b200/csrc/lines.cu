@@ -282,7 +282,7 @@ cudaError_t launch_lines(int which, int N, const LinesArgs& a, int T, cudaStream
         case 512: return launch_lines_n<512, 8>(which, a, T, s);
         case 1024: return launch_lines_n<1024, 4>(which, a, T, s);
     }
-    return cudaErrorInvalidValue;
+    return cudaErrorNotSupported;  // no line-FFT instantiation for this side
 }
 
 cudaError_t launch_build_pupils(float2* pupils, const uint8_t* support, const double* defocus, int n, int T,
