@@ -103,3 +103,22 @@ def test_config3_full_fov_physical_parity(orc):
         amp, ph = amp_phase_rel(got.tiles[t], ref.hr)
         assert amp < 1e-3 and ph < 1e-3, (t, amp, ph)
         assert np.allclose(got.tile_metrics[t].pass_mean_residual, ref.residuals, rtol=1e-3)
+
+
+@pytest.mark.gpu
+def test_acceptance_round_trip_recovery_on_device(orc):
+    """Acceptance criterion 1 (acceptance.cpp:99-121) on the device: stock
+    geometry (256-px tile, upsample 4, 9x9 LEDs), composite object, 5 GS
+    iterations; the globally aligned reconstruction against the band-limited
+    truth must reach amplitude RMSE <= 0.03 and phase RMSE <= 0.1 rad."""
+    cfg = fpm.OpticalConfig(led_scan_rows=9, led_scan_cols=9)
+    oc = orc_cfg(cfg)
+    obj = orc.synth_object("composite", 1024, 1)
+    seq = orc.led_sequence("spiral", oc)
+    fs = simulate_dataset(obj, seq, cfg, device="cuda")
+    t = fpm.partition_tiles(fs.width(), fs.height(), cfg)[0]
+    res = fpm.reconstruct_tile(fs, t, cfg, 5, seq)
+    truth = orc.band_limit(obj, fpm.synthesized_na(cfg), oc)
+    aligned = res.hr.astype(np.complex128) * orc.global_alignment(res.hr, truth)
+    arms, prms = orc.rmse(aligned, truth)
+    assert arms <= 0.03 and prms <= 0.1, (arms, prms)
