@@ -122,3 +122,46 @@ def test_acceptance_round_trip_recovery_on_device(orc):
     aligned = res.hr.astype(np.complex128) * orc.global_alignment(res.hr, truth)
     arms, prms = orc.rmse(aligned, truth)
     assert arms <= 0.03 and prms <= 0.1, (arms, prms)
+
+
+def _bar_groups(size):
+    """USAF-like bar groups of the Bars object (forward.cpp:22-40)."""
+    out = []
+    band = size // 5
+    for g, p in enumerate((64, 32, 16, 8, 4)):
+        start = size // 2 - (5 * p) // 4
+        out.append(dict(period=p, row=(g * band + band // 4 + g * band + 3 * band // 4) // 2,
+                        bars=[start + b * p + p // 4 for b in range(3)],
+                        gaps=[start + b * p + (3 * p) // 4 for b in range(2)]))
+    return out
+
+
+def _min_resolved_period(amp, size, scale):
+    """Smallest bar period with contrast >= 0.2 (acceptance.cpp:57-73)."""
+    best = 1 << 20
+    for g in _bar_groups(size):
+        row = g["row"] // scale
+        bar = np.mean([amp[row, x // scale] for x in g["bars"]])
+        gap = np.mean([amp[row, x // scale] for x in g["gaps"]])
+        if (gap - bar) / (gap + bar) >= 0.2:
+            best = min(best, g["period"])
+    return best
+
+
+@pytest.mark.gpu
+def test_acceptance_resolution_gain_on_device(orc):
+    """Acceptance criterion 2 (acceptance.cpp:125-145) on the device: the Bars
+    object under the stock 13x13 scan; the reconstruction (3 GS iterations)
+    must resolve bars at most half the period the on-axis LR frame resolves."""
+    cfg = fpm.OpticalConfig()
+    oc = orc_cfg(cfg)
+    obj = orc.synth_object("bars", 1024, 0)
+    seq = orc.led_sequence("spiral", oc)
+    fs = simulate_dataset(obj, seq, cfg, device="cuda")
+    lr_amp = np.sqrt(fs.images[fs.find(cfg.center_led)].astype(np.float64))
+    lr_min = _min_resolved_period(lr_amp, 1024, cfg.upsample)
+    t = fpm.partition_tiles(fs.width(), fs.height(), cfg)[0]
+    res = fpm.reconstruct_tile(fs, t, cfg, 3, seq)
+    hr_min = _min_resolved_period(np.abs(res.hr), 1024, 1)
+    assert lr_min < (1 << 20), "no bars resolved in the LR frame"
+    assert 2 * hr_min <= lr_min, (lr_min, hr_min)
