@@ -63,3 +63,19 @@ def test_online_epry_equals_offline(eng, n):
     on = fpm.run_online(fs, cfg, seq, opt, 0.0, engine=eng, stitch=False)
     assert np.array_equal(on.tiles, off.tiles)
     assert np.array_equal(on.pupils, off.pupils)
+
+
+@pytest.mark.gpu
+def test_online_wall_tracks_acquisition(eng):
+    """Acceptance criterion 5 (acceptance.cpp:247-268) at 20x replay speed: 169
+    frames at the 0.33 s cadence; the device keeps up, so the wall time stays
+    within 10% of the acquisition time (per-frame work << the frame period)."""
+    import time
+    cfg = gpu_cfg(led_scan_rows=13, led_scan_cols=13)
+    fs, _, seq, _ = dataset(cfg, seed=5)
+    assert len(seq) == 169
+    t0 = time.perf_counter()
+    res = fpm.run_online(fs, cfg, seq, fpm.RunOptions(iters=1), 0.05, engine=eng)
+    wall = time.perf_counter() - t0
+    assert res.acquisition_s == pytest.approx(169 * 0.33 * 0.05)
+    assert abs(wall - res.acquisition_s) <= 0.1 * res.acquisition_s, (wall, res.acquisition_s)
