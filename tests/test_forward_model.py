@@ -165,3 +165,32 @@ def test_acceptance_resolution_gain_on_device(orc):
     hr_min = _min_resolved_period(np.abs(res.hr), 1024, 1)
     assert lr_min < (1 << 20), "no bars resolved in the LR frame"
     assert 2 * hr_min <= lr_min, (lr_min, hr_min)
+
+
+def _seam_phase_jump(f, seam, vertical):
+    """Mean |wrapped phase step| across a seam (metrics.cpp:59-85)."""
+    a = np.angle(f[:, seam]) - np.angle(f[:, seam - 1]) if vertical else \
+        np.angle(f[seam, :]) - np.angle(f[seam - 1, :])
+    return float(np.mean(np.abs((a + np.pi) % (2 * np.pi) - np.pi)))
+
+
+@pytest.mark.gpu
+def test_acceptance_stitch_continuity_on_device(orc):
+    """Acceptance criterion 6 (acceptance.cpp:272-308) on the device: 2x2 tiles
+    of 256 px, 5x5 LEDs, 3 iterations; the Eq. (1) mosaic with a 26-px overlap
+    must cut the seam phase jump below 0.2x that of the overlap-free mosaic,
+    and 256 + 256 - 26 = 486 must hold for the mosaic width."""
+    def stitched_for(overlap, fov):
+        cfg = fpm.OpticalConfig(led_scan_rows=5, led_scan_cols=5, tile_overlap=overlap)
+        oc = orc_cfg(cfg)
+        obj = orc.synth_object("composite", fov * cfg.upsample, 9)
+        seq = orc.led_sequence("spiral", oc)
+        fs = simulate_dataset(obj, seq, cfg, device="cuda")
+        return fpm.run_offline(fs, cfg, seq, fpm.RunOptions(iters=3)).stitched
+
+    with_ov, no_ov = stitched_for(26, 486), stitched_for(0, 512)
+    up = 4
+    assert with_ov.shape == (486 * up, 486 * up)
+    jump_ov = 0.5 * (_seam_phase_jump(with_ov, 243 * up, True) + _seam_phase_jump(with_ov, 243 * up, False))
+    jump_no = 0.5 * (_seam_phase_jump(no_ov, 256 * up, True) + _seam_phase_jump(no_ov, 256 * up, False))
+    assert jump_ov < 0.2 * jump_no, (jump_ov, jump_no)
