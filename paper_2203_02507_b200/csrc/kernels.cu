@@ -144,7 +144,7 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
     }
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        const float4 w = W4_s[(tc * (4 * h + m)) & 63];
+        const float4 w = W4_s[64 + (m * 2 + h) * 8 + tc];  // = W64^(tc (4h + m)), lane-consecutive
 #pragma unroll
         for (int a = 0; a < 8; ++a) v[a][m] = cmul_sw(v[a][m], make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
@@ -213,7 +213,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
     size_t b = 1024;                                              // alignment slack (128B-swizzled TMA box)
     b += size_t(G) * kGroupBytes;                                 // per-group staging + transpose
     b += size_t(nslots) * kGroupThreads * sizeof(float2);         // lattice pupil [NP][128]
-    b += 64 * sizeof(float4);                                     // W64 table (+ swizzled copy)
+    b += 128 * sizeof(float4);                                    // W64 table + column-twiddle table
     b += size_t(iters) * sizeof(double);                          // stage sums
     b += size_t(G) * (sizeof(uint64_t) + 16 * sizeof(float));     // mbarriers + reductions
     b += size_t(L) * (sizeof(short2) + sizeof(int) + sizeof(float) + 1);  // origins, frame map, sum(I), bright flags
@@ -242,8 +242,10 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     size_t off = size_t(G) * kGroupBytes;
     float2* P_s = reinterpret_cast<float2*>(smem + off);  // [NP][128], P' = (-1)^(i+j) P, zero off the support
     off += size_t(NP) * kGroupThreads * sizeof(float2);
-    float4* W4_s = reinterpret_cast<float4*>(smem + off);  // (W64^m, swizzled W64^m), m in [0, 64)
-    off += 64 * sizeof(float4);
+    // [0, 64): (W64^m, swizzled), m in [0, 64); [64, 128): the column twiddle W64^(tc (4h + m))
+    // at 64 + (m 2 + h) 8 + tc, so the 16 (tc, h) lanes of a quarter-warp read consecutive entries
+    float4* W4_s = reinterpret_cast<float4*>(smem + off);
+    off += 128 * sizeof(float4);
     double* stage_sum = reinterpret_cast<double*>(smem + off);
     off += size_t(args.iters) * sizeof(double);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off);
@@ -281,10 +283,12 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
         B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
     }
     for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
-    if (threadIdx.x < 64) {
+    if (threadIdx.x < 128) {
+        const int t = threadIdx.x, e = t - 64;
+        const int m = t < 64 ? t : (((e & 7) * (4 * ((e >> 3) & 1) + (e >> 4))) & 63);
         double s, c;
-        sincospi(-double(threadIdx.x) / 32.0, &s, &c);
-        W4_s[threadIdx.x] = make_float4(float(c), float(s), -float(s), float(c));
+        sincospi(-double(m) / 32.0, &s, &c);
+        W4_s[t] = make_float4(float(c), float(s), -float(s), float(c));
     }
     // pair-combine twiddles W8^m, m = 1..3, on the odd lane (1 on the even lane)
     float2 tw[4];
