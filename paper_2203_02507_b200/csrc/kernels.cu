@@ -144,7 +144,7 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
     }
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        const float4 w = W4_s[64 + (m * 2 + h) * 8 + tc];  // = W64^(tc (4h + m)), lane-consecutive
+        const float4 w = W4_s[64 + m * 16 + 2 * tc + h];  // = W64^(tc (4h + m)), in lane order
 #pragma unroll
         for (int a = 0; a < 8; ++a) v[a][m] = cmul_sw(v[a][m], make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     float2* P_s = reinterpret_cast<float2*>(smem + off);  // [NP][128], P' = (-1)^(i+j) P, zero off the support
     off += size_t(NP) * kGroupThreads * sizeof(float2);
     // [0, 64): (W64^m, swizzled), m in [0, 64); [64, 128): the column twiddle W64^(tc (4h + m))
-    // at 64 + (m 2 + h) 8 + tc, so the 16 (tc, h) lanes of a quarter-warp read consecutive entries
+    // at 64 + 16 m + 2 tc + h, i.e. in lane order (lane = 2 (8 tr + tc) + h): conflict-free
     float4* W4_s = reinterpret_cast<float4*>(smem + off);
     off += 128 * sizeof(float4);
     double* stage_sum = reinterpret_cast<double*>(smem + off);
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
     if (threadIdx.x < 128) {
         const int t = threadIdx.x, e = t - 64;
-        const int m = t < 64 ? t : (((e & 7) * (4 * ((e >> 3) & 1) + (e >> 4))) & 63);
+        const int m = t < 64 ? t : ((((e & 15) >> 1) * (4 * (e & 1) + (e >> 4))) & 63);
         double s, c;
         sincospi(-double(m) / 32.0, &s, &c);
         W4_s[t] = make_float4(float(c), float(s), -float(s), float(c));
