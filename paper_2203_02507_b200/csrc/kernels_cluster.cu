@@ -3,25 +3,26 @@
 // the LED loop. Same arithmetic as fpm_loop_box (kernels_box.cu), so the two
 // produce the same canvas bit for bit; what changes is where the work runs:
 //
-//   A  rows i = b0 + rank + CL t of the pupil box: gather the disk x P', IFFT
-//      (warp F2), and scatter each row's n outputs to the CTA owning those
-//      columns — column slab c holds columns [c n/CL, (c+1) n/CL) of all B box
-//      rows (DSMEM stores, 32 consecutive elements per lane group)
-//   -- cluster barrier --
+//   A  the CTA's box rows (row i belongs to CTA (o.x + i) mod CL: ownership by
+//      absolute canvas row): gather the disk x P', IFFT (warp F2), send each
+//      row's n outputs to the CTAs owning those columns — column slab c holds
+//      columns [c n/CL, (c+1) n/CL) of all B box rows. n <= 128: st.async into
+//      the owner's shared memory, counted in bytes on its mbarrier; n = 256:
+//      DSMEM stores + cluster barrier
 //   B  the CTA's own columns: IFFT over the box rows (F1) -> modulus with
-//      sqrt(I) -> FFT (F2) -> keep the box rows; the measurement slab is staged
-//      column-major with rows permuted (k0, t) so the modulus reads are
-//      conflict-free
+//      sqrt(I) -> FFT (F2) -> keep the box rows; the measurement slab (staged
+//      one update ahead by cp.async, pair-XOR swizzled) gives conflict-free
+//      modulus reads
 //   -- cluster barrier -- (residual and EPRY maxima reduced over the cluster)
 //   C  the same rows as A: fetch the row from the column slabs (DSMEM loads),
 //      FFT (F1), scatter into the canvas disk (GS / EPRY)
-//   -- cluster barrier -- (slabs free; canvas writes visible cluster-wide)
+//   -- CTA barrier (a canvas row's next reader may be another warp of the
+//      CTA); a cluster barrier only after a pupil step (pupil rows move with the
+//      box rows) or, with a single slab buffer (n = 256), to free the slabs
 //
-// A row's canvas disk moves with the LED, so consecutive updates read canvas
-// rows another CTA of the cluster wrote: the third barrier (release/acquire at
-// cluster scope) orders them. Use: n = 256 tiles, whose B x n intermediate
-// (240 KB) does not fit one SM, and single-tile runs, where one CTA would
-// leave 147 SMs idle (BASELINE configs 1-2).
+// Slabs and partial sums are double-buffered for n <= 128. Use: n = 256
+// tiles, whose B x n intermediate (240 KB) does not fit one SM, and
+// single-tile runs, where one CTA would leave 147 SMs idle (BASELINE config 2).
 #include <cooperative_groups.h>
 
 #include "kernels.cuh"
