@@ -248,6 +248,8 @@ struct fpmgpu_plan {
     DevBuf<int> seq_frame;
     DevBuf<int2> tile_xy, slots;
     DevBuf<double> defocus, resid;
+    DevBuf<int> work;     // LED-loop work queue: item counter + per-tile passes done
+    DevBuf<float> isum;   // [T][L] sum(I) per crop (work-queue items of later passes)
     bool has_defocus = false, has_pupils = false;
     // phase events of recent executes: [slot][4] = start, after init, after loop, after finalize
     static constexpr int kEventSlots = 256;
@@ -469,6 +471,10 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
             ck(fpmk::launch_loop_box(p.n, r.mode, a, bx, p.T, s), "LED loop (box)");
     } else {
         const CUtensorMap map = encode_frames_map(frames, p.F, r.height, r.width, pitch);
+        if (p.G == 1 && s0 == 0 && s1 == p.num_slots && !acc) {  // whole run: the work queue may serve it
+            a.work = p.work.ensure(size_t(p.T) + 1);
+            a.isum = p.isum.ensure(size_t(p.T) * p.L);
+        }
         ck(fpmk::launch_loop64(r.mode, p.prune, fpmk::kMeasTMA, p.G, &map, a, p.T, s), "LED loop");
     }
 }

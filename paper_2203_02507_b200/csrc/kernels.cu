@@ -25,6 +25,9 @@
 //
 // The centred transforms use fft2(x) = C . FFT(C . x), C = (-1)^(i+j)
 // (field.cpp:48-87); C is constant per thread and folded into the shared pupil.
+#include <algorithm>
+#include <cstdlib>
+
 #include "fft_device.cuh"
 #include "kernels.cuh"
 
@@ -78,6 +81,15 @@ __device__ __forceinline__ void tma_load_crop(void* dst, const CUtensorMap* map,
         " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(f)
         : "memory");
+}
+
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // Barrier over one 128-thread group (named barrier 1 + g).
@@ -217,6 +229,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
     b += size_t(iters) * sizeof(double);                          // stage sums
     b += size_t(G) * (sizeof(uint64_t) + 16 * sizeof(float));     // mbarriers + reductions
     b += size_t(L) * (sizeof(short2) + sizeof(int) + sizeof(float) + 1);  // origins, frame map, sum(I), bright flags
+    b += 8;                                                       // work-queue item (4-byte aligned)
     return b;
 }
 
@@ -234,7 +247,6 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     const int p = tl >> 1, h = tl & 1;
     const int tr = p >> 3, tc = p & 7;
     const int warp = tl >> 5;
-    const int tile = blockIdx.x;
     const int L = args.L;
 
     uint16_t* I_s = reinterpret_cast<uint16_t*>(smem + g * kGroupBytes);
@@ -259,30 +271,13 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     float* D_s = reinterpret_cast<float*>(smem + off);  // sum(I) per LED, formed on its first visit
     off += size_t(L) * sizeof(float);
     uint8_t* B_s = smem + off;
+    off += size_t(L);
+    off = (off + 3) & ~size_t(3);
+    int* item_s = reinterpret_cast<int*>(smem + off);  // work queue: the CTA's current item
     uint64_t* bar = bars + g;
     float* rg = red + g * 16;
 
-    float2* canvas = args.canvas + size_t(tile) * N * N;
-    float2* pupil_g = args.pupils + size_t(tile) * 64 * 64;
-    const int2 txy = args.tile_xy[tile];
-    const float sgn = ((tr + tc) & 1) ? -1.f : 1.f;  // checkerboard (-1)^(i+j), constant per thread
-    const float sgn_eps = sgn * 0x1p-60f;            // see the modulus replacement
-
-    // ---- one-time setup: support mask, lattice pupil, tables, W64 table
-    uint32_t mask = 0;
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-        const int i = tr + 8 * Lat::a(q), jj = tc + 8 * (2 * Lat::j(q) + h);
-        const bool on = args.support[i * 64 + jj] != 0;
-        mask |= uint32_t(on) << q;
-        if (g == 0) P_s[q * kGroupThreads + tl] = on ? cscale(pupil_g[i * 64 + jj], sgn) : make_float2(0.f, 0.f);
-    }
-    for (int k = threadIdx.x; k < L; k += blockDim.x) {
-        O_s[k] = args.origins[size_t(tile) * L + k];
-        F_s[k] = args.seq_frame[k];
-        B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
-    }
-    for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
+    // ---- one-time setup: W64 tables, pair twiddles, mbarrier
     if (threadIdx.x < 128) {
         const int t = threadIdx.x, e = t - 64;
         const int m = t < 64 ? t : ((((e & 15) >> 1) * (4 * (e & 1) + (e >> 4))) & 63);
@@ -307,10 +302,74 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
-
+    const float sgn = ((tr + tc) & 1) ? -1.f : 1.f;  // checkerboard (-1)^(i+j), constant per thread
+    const float sgn_eps = sgn * 0x1p-60f;            // see the modulus replacement
     const float inv_n2 = 1.0f / 4096.0f;  // ifft2's 1/(rows*cols) (field.cpp:64-66)
     uint32_t phase = 0;
+    // canvas offset of lattice position (a, j) relative to the sub-aperture origin
+    const int cbase = tr * N + tc + 8 * h;
+    // work queue (G == 1): items j = it * T + tile in iteration-major order; item j
+    // depends on item j - T (the tile's previous pass), claimed 1.7 waves earlier at
+    // BASELINE config 3, so the dependency wait is almost never taken. Every update
+    // runs the same instructions as in the one-CTA-per-tile launch: bit-identical
+    const bool queue = G == 1 && args.work != nullptr;
+    const int n_items = args.T * args.iters;
+    int prev_tile = -1, prev_it = 0;
+
+    for (int round = 0;; ++round) {
+    int tile, it_q = 0, s_begin, s_end;
+    if (queue) {
+        __syncthreads();  // the previous item's stores (canvas, pupil, residual, sum(I)) are done
+        if (threadIdx.x == 0) {
+            if (prev_tile >= 0) {  // release: publish the finished pass
+                __threadfence();
+                st_release_gpu(args.work + 1 + prev_tile, prev_it + 1);
+            }
+            const int j = atomicAdd(args.work, 1);
+            *item_s = j;
+            if (j < n_items && j >= args.T) {  // acquire: the tile's previous pass is complete
+                const int* flag = args.work + 1 + (j % args.T);
+                while (ld_acquire_gpu(flag) < j / args.T) __nanosleep(256);
+                __threadfence();
+            }
+        }
+        __syncthreads();
+        const int j = *item_s;
+        if (j >= n_items) break;
+        tile = j % args.T;
+        it_q = j / args.T;
+        s_begin = it_q * L;
+        s_end = s_begin + L;
+        prev_tile = tile;
+        prev_it = it_q;
+    } else {
+        if (round > 0) break;
+        tile = blockIdx.x;
+        s_begin = args.slot_begin;
+        s_end = args.num_slots;
+    }
+
+    // ---- per-tile setup: support mask, lattice pupil, origins, frame map, flags
+    float2* canvas = args.canvas + size_t(tile) * N * N;
+    float2* pupil_g = args.pupils + size_t(tile) * 64 * 64;
+    const int2 txy = args.tile_xy[tile];
+    uint32_t mask = 0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        const int i = tr + 8 * Lat::a(q), jj = tc + 8 * (2 * Lat::j(q) + h);
+        const bool on = args.support[i * 64 + jj] != 0;
+        mask |= uint32_t(on) << q;
+        if (g == 0) P_s[q * kGroupThreads + tl] = on ? cscale(pupil_g[i * 64 + jj], sgn) : make_float2(0.f, 0.f);
+    }
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+        O_s[k] = args.origins[size_t(tile) * L + k];
+        F_s[k] = args.seq_frame[k];
+        B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
+        if (queue && it_q > 0) D_s[k] = args.isum[size_t(tile) * L + k];
+    }
+    for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
+    __syncthreads();
+
     bool issued = false;
     bool pupil_dirty = true;  // EPRY: max|P|^2 changes only after a pupil step
     auto issue = [&](int2 e) {
@@ -319,10 +378,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
             tma_load_crop(I_s, &tmap, bar, txy.x, txy.y, F_s[e.y]);
         }
     };
-    // canvas offset of lattice position (a, j) relative to the sub-aperture origin
-    const int cbase = tr * N + tc + 8 * h;
-
-    for (int s = args.slot_begin; s < args.num_slots; ++s) {
+    for (int s = s_begin; s < s_end; ++s) {
         const int2 e = slot_entry<G>(args, s, g);
         if (e.x >= 0) {
             if (!issued) issue(e);
@@ -383,7 +439,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
                 phase ^= 1u;
             }
             // sum(I) of an LED's crop is formed once, on its first visit in this launch
-            const bool first = G == 1 ? s - args.slot_begin < L : e.x == 0;
+            const bool first = queue ? it_q == 0 : G == 1 ? s - args.slot_begin < L : e.x == 0;
             float num = 0.f, den_f = 0.f;
             uint32_t den_u = 0;
 #pragma unroll
@@ -429,7 +485,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
             group_sync(g);  // staging and transpose buffers free; reductions visible
 
             // prefetch the measurement of this group's next update
-            if (s + 1 < args.num_slots) {
+            if (s + 1 < s_end) {
                 const int2 nx = slot_entry<G>(args, s + 1, g);
                 if (nx.x >= 0) {
                     issue(nx);
@@ -489,22 +545,56 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     }
 
     // ---- per-pass mean residual; EPRY pupil back to global
-    store_residuals(args, tile, stage_sum, G == 1);
+    if (queue) {
+        if (threadIdx.x == 0) args.residuals[size_t(tile) * args.iters + it_q] = stage_sum[it_q] / double(L);
+        if (it_q == 0)
+            for (int k = threadIdx.x; k < L; k += blockDim.x) args.isum[size_t(tile) * L + k] = D_s[k];
+    } else {
+        store_residuals(args, tile, stage_sum, G == 1);
+    }
     if (MODE == kModeEPRY && g == 0) {
 #pragma unroll
         for (int q = 0; q < NP; ++q)
             if ((mask >> q) & 1u)
                 pupil_g[(tr + 8 * Lat::a(q)) * 64 + tc + 8 * (2 * Lat::j(q) + h)] = cscale(P_s[q * kGroupThreads + tl], sgn);
     }
+    }  // items
+}
+
+// FPM_B200_QUEUE: unset = work queue when the tiles exceed the resident CTAs;
+// 0 = never; 1 = always (tests: a grid wider than the tile count exercises the
+// dependency waits)
+static int queue_override() {
+    const char* e = std::getenv("FPM_B200_QUEUE");
+    return e && e[0] ? (e[0] == '1' ? 1 : 0) : -1;
 }
 
 template <int MODE, bool PRUNE, int MEAS, int G, int N>
-static cudaError_t launch_loop_t(const CUtensorMap* tmap, const LoopArgs& a, int T, cudaStream_t s) {
-    const size_t smem = loop_smem_bytes(G, a.nslots, a.L, a.iters);
+static cudaError_t launch_loop_t(const CUtensorMap* tmap, const LoopArgs& a0, int T, cudaStream_t s) {
+    const size_t smem = loop_smem_bytes(G, a0.nslots, a0.L, a0.iters);
     auto k = fpm_loop64<MODE, PRUNE, MEAS, G, N>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    k<<<T, kGroupThreads * G, smem, s>>>(*tmap, a);
+    LoopArgs a = a0;
+    int grid = T;
+    const int q = queue_override();
+    if (G == 1 && a.work && a.isum && q != 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kGroupThreads * G, smem)) != cudaSuccess)
+            return e;
+        const int resident = std::max(1, per_sm * sms);
+        if (T > resident || q == 1) {
+            grid = q == 1 ? std::min(resident, T * a.iters) : resident;
+            if ((e = cudaMemsetAsync(a.work, 0, sizeof(int) * size_t(T + 1), s)) != cudaSuccess) return e;
+        } else {
+            a.work = nullptr;
+        }
+    } else {
+        a.work = nullptr;
+    }
+    k<<<grid, kGroupThreads * G, smem, s>>>(*tmap, a);
     return cudaGetLastError();
 }
 

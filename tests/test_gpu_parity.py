@@ -308,6 +308,31 @@ def test_banded_host_path_bit_identical(eng, monkeypatch, bands):
         assert np.array_equal(pa, pb)
 
 
+@pytest.mark.parametrize("mode", ["gs", "epry"])
+def test_work_queue_bit_identical(eng, monkeypatch, mode):
+    """The n = 64 LED loop as a persistent work queue over (pass, tile) items
+    (FPM_B200_QUEUE=1 forces it, with a grid wider than the tile count, so most
+    items wait on their tile's previous pass held by another CTA) gives the
+    one-CTA-per-tile launch's tiles, residuals and pupils bit for bit."""
+    cfg = gpu_cfg(led_scan_rows=7, led_scan_cols=7, tile_overlap=8)
+    fs, _, seq, _ = dataset(cfg, fov=232, seed=35)
+    specs = fpm.partition_tiles(fs.width(), fs.height(), cfg)
+    rng = np.random.default_rng(5)
+    opt = fpm.RunOptions(iters=3, mode=mode, tile_defocus_um=list(rng.uniform(-8, 8, len(specs))))
+    monkeypatch.setenv("FPM_B200_BANDS", "1")
+    monkeypatch.setenv("FPM_B200_QUEUE", "0")
+    a = fpm.run_offline(fs, cfg, seq, opt, engine=eng, stitch=False)
+    monkeypatch.setenv("FPM_B200_QUEUE", "1")
+    b = fpm.run_offline(fs, cfg, seq, opt, engine=eng, stitch=False)
+    assert len(specs) == 16
+    assert np.array_equal(a.tiles, b.tiles)
+    assert np.array_equal(np.array([m.pass_mean_residual for m in a.tile_metrics]),
+                          np.array([m.pass_mean_residual for m in b.tile_metrics]))
+    if mode == "epry":
+        for pa, pb in zip(a.pupils, b.pupils):
+            assert np.array_equal(pa, pb)
+
+
 @pytest.mark.parametrize("n,cl,mode", [(128, 2, "epry"), (128, 4, "gs"), (128, 8, "epry"), (128, 16, "gs"), (256, 2, "gs"),
                                        (256, 4, "epry"), (256, 8, "gs")])
 def test_cluster_kernel_matches_box_kernel(eng, monkeypatch, n, cl, mode):
