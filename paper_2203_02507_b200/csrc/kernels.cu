@@ -26,6 +26,7 @@
 // The centred transforms use fft2(x) = C . FFT(C . x), C = (-1)^(i+j)
 // (field.cpp:48-87); C is constant per thread and folded into the shared pupil.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "fft_device.cuh"
@@ -308,28 +309,32 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     uint32_t phase = 0;
     // canvas offset of lattice position (a, j) relative to the sub-aperture origin
     const int cbase = tr * N + tc + 8 * h;
-    // work queue (G == 1): items j = it * T + tile in iteration-major order; item j
-    // depends on item j - T (the tile's previous pass), claimed 1.7 waves earlier at
-    // BASELINE config 3, so the dependency wait is almost never taken. Every update
-    // runs the same instructions as in the one-CTA-per-tile launch: bit-identical
+    // work queue (G == 1): items j = (it * H + part) * T + tile, H = parts per pass
+    // (LED positions [part L / H, (part + 1) L / H) of pass it); item j depends on
+    // item j - T (the tile's previous part), claimed 1.7 waves earlier at BASELINE
+    // config 3, so the dependency wait is almost never taken. Every update runs the
+    // same instructions as in the one-CTA-per-tile launch, and a part continues the
+    // pass's residual sum where the previous part left it (stored unscaled in the
+    // residual slot): bit-identical
     const bool queue = G == 1 && args.work != nullptr;
-    const int n_items = args.T * args.iters;
-    int prev_tile = -1, prev_it = 0;
+    const int H = queue ? args.parts : 1;
+    const int n_items = args.T * args.iters * H;
 
     for (int round = 0;; ++round) {
-    int tile, it_q = 0, s_begin, s_end;
+    int tile, it_q = 0, part = 0, s_begin, s_end;
     if (queue) {
         __syncthreads();  // the previous item's stores (canvas, pupil, residual, sum(I)) are done
         if (threadIdx.x == 0) {
-            if (prev_tile >= 0) {  // release: publish the finished pass
+            if (round > 0) {  // release: publish the finished item (item_s still holds it)
+                const int jp = *item_s;
                 __threadfence();
-                st_release_gpu(args.work + 1 + prev_tile, prev_it + 1);
+                st_release_gpu(args.work + 1 + jp % args.T, jp / args.T + 1);
             }
             const int j = atomicAdd(args.work, 1);
             *item_s = j;
             if (j < n_items && j >= args.T) {  // acquire: the tile's previous pass is complete
                 const int* flag = args.work + 1 + (j % args.T);
-                while (ld_acquire_gpu(flag) < j / args.T) __nanosleep(256);
+                while (ld_acquire_gpu(flag) < j / args.T) __nanosleep(256);  // items of the tile done
                 __threadfence();
             }
         }
@@ -337,11 +342,11 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
         const int j = *item_s;
         if (j >= n_items) break;
         tile = j % args.T;
-        it_q = j / args.T;
-        s_begin = it_q * L;
-        s_end = s_begin + L;
-        prev_tile = tile;
-        prev_it = it_q;
+        const int ip = j / args.T;  // it * H + part
+        it_q = ip / H;
+        part = ip % H;
+        s_begin = it_q * L + part * L / H;
+        s_end = it_q * L + (part + 1) * L / H;
     } else {
         if (round > 0) break;
         tile = blockIdx.x;
@@ -367,7 +372,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
         B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
         if (queue && it_q > 0) D_s[k] = args.isum[size_t(tile) * L + k];
     }
-    for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
+    for (int k = threadIdx.x; k < args.iters; k += blockDim.x)
+        stage_sum[k] = queue && part > 0 && k == it_q ? args.residuals[size_t(tile) * args.iters + k] : 0.0;
     __syncthreads();
 
     bool issued = false;
@@ -546,9 +552,10 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
 
     // ---- per-pass mean residual; EPRY pupil back to global
     if (queue) {
-        if (threadIdx.x == 0) args.residuals[size_t(tile) * args.iters + it_q] = stage_sum[it_q] / double(L);
+        if (threadIdx.x == 0)  // a pass's last part stores the mean, earlier parts the running sum
+            args.residuals[size_t(tile) * args.iters + it_q] = part == H - 1 ? stage_sum[it_q] / double(L) : stage_sum[it_q];
         if (it_q == 0)
-            for (int k = threadIdx.x; k < L; k += blockDim.x) args.isum[size_t(tile) * L + k] = D_s[k];
+            for (int k = s_begin + int(threadIdx.x); k < s_end; k += blockDim.x) args.isum[size_t(tile) * L + k] = D_s[k];
     } else {
         store_residuals(args, tile, stage_sum, G == 1);
     }
@@ -586,7 +593,20 @@ static cudaError_t launch_loop_t(const CUtensorMap* tmap, const LoopArgs& a0, in
             return e;
         const int resident = std::max(1, per_sm * sms);
         if (T > resident || q == 1) {
-            grid = q == 1 ? std::min(resident, T * a.iters) : resident;
+            // parts per pass: the fewest (<= 4) that fill the last round of items best
+            const double items = double(T) * a.iters;
+            double best = 0.0;
+            a.parts = 1;
+            for (int h = 1; h <= 4 && h <= a.L; ++h) {
+                const double rounds = items * h / resident;
+                const double fill = rounds / std::ceil(rounds);
+                if (fill > best + 0.005) {
+                    best = fill;
+                    a.parts = h;
+                }
+            }
+            if (const char* pe = std::getenv("FPM_B200_PARTS"); pe && pe[0]) a.parts = std::max(1, std::min(a.L, std::atoi(pe)));
+            grid = q == 1 ? std::min(resident, T * a.iters * a.parts) : resident;
             if ((e = cudaMemsetAsync(a.work, 0, sizeof(int) * size_t(T + 1), s)) != cudaSuccess) return e;
         } else {
             a.work = nullptr;

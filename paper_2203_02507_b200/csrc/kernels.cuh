@@ -29,10 +29,11 @@ struct LoopArgs {
     int T, L, iters, N, nslots;
     float alpha, beta;        // EPRY step sizes
     // Work queue (G == 1, whole runs, more tiles than resident CTAs): a persistent
-    // grid pulls (iteration, tile) items in iteration-major order; work[0] is the
-    // item counter, work[1 + t] the passes tile t has completed (zeroed per launch)
+    // grid pulls (pass, part, tile) items in that order; work[0] is the item
+    // counter, work[1 + t] the items of tile t completed (zeroed per launch)
     int* work;                // nullptr: one CTA per tile, the whole slot range
     float* isum;              // [T][L] sum(I) of each LED's crop, formed by the pass-0 items
+    int parts;                // work queue: items per pass (a pass's LED range cut into parts)
 };
 
 // Line FFTs for init_canvas / canvas_to_field (K2 / K3).

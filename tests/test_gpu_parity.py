@@ -308,12 +308,13 @@ def test_banded_host_path_bit_identical(eng, monkeypatch, bands):
         assert np.array_equal(pa, pb)
 
 
-@pytest.mark.parametrize("mode", ["gs", "epry"])
-def test_work_queue_bit_identical(eng, monkeypatch, mode):
-    """The n = 64 LED loop as a persistent work queue over (pass, tile) items
-    (FPM_B200_QUEUE=1 forces it, with a grid wider than the tile count, so most
-    items wait on their tile's previous pass held by another CTA) gives the
+@pytest.mark.parametrize("mode,parts", [("gs", "1"), ("epry", "3"), ("epry", "")])
+def test_work_queue_bit_identical(eng, monkeypatch, mode, parts):
+    """The n = 64 LED loop as a persistent work queue over (pass, part, tile)
+    items (FPM_B200_QUEUE=1 forces it, with a grid wider than the tile count, so
+    most items wait on their tile's previous part held by another CTA) gives the
     one-CTA-per-tile launch's tiles, residuals and pupils bit for bit."""
+    monkeypatch.setenv("FPM_B200_PARTS", parts)
     cfg = gpu_cfg(led_scan_rows=7, led_scan_cols=7, tile_overlap=8)
     fs, _, seq, _ = dataset(cfg, fov=232, seed=35)
     specs = fpm.partition_tiles(fs.width(), fs.height(), cfg)
