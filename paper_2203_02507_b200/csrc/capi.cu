@@ -180,6 +180,14 @@ int cluster_choice(int n, int N, int T) {
     return 0;
 }
 
+// FPM_B200_W64=1 runs n = 64 one warp per tile (kernels_w64.cu). Opt-in: at 8
+// warps per SM it is latency- and instruction-cache-bound (config 3 loop 148 ms
+// vs 32 ms for the 128-thread lattice kernel).
+bool w64_choice(int /*T*/) {
+    const char* e = std::getenv("FPM_B200_W64");
+    return e && e[0] == '1';
+}
+
 std::vector<float2> twiddles(int N) {
     std::vector<float2> w(static_cast<size_t>(N));
     for (int m = 0; m < N; ++m) {
@@ -236,6 +244,7 @@ struct fpmgpu_plan {
     int n = 0, N = 0, T = 0, L = 0, F = 0, G = 1, lag = 0, nslots = 1, num_slots = 0;
     bool prune = false;
     bool use_box = false;  // n != 64: warp-FFT box kernel (kernels_box.cu)
+    bool w64 = false;      // n = 64, sequential, disk inside [16, 48): one warp per tile (kernels_w64.cu)
     int cl = 0;            // > 0: each tile split over a cluster of cl CTAs (kernels_cluster.cu)
     int box = 0, b0 = 0;
     int support_px = 0;
@@ -378,6 +387,8 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
         }
     }
     p.num_slots = p.G == 1 ? r.iters * p.L : int(slots.size() / 2);
+    p.w64 = !p.use_box && !p.cl && p.prune && p.G == 1 && w64_choice(p.T) &&
+            fpmk::loop_w64_smem_bytes(p.L, r.iters) <= 227 * 1024;
 
     cudaStream_t s = p.ctx->stream;
     p.support.upload(sup.data(), sup.size(), s);
@@ -469,6 +480,16 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
             ck(fpmk::launch_loop_cluster(p.n, r.mode, p.cl, a, bx, p.T, s), "LED loop (cluster)");
         else
             ck(fpmk::launch_loop_box(p.n, r.mode, a, bx, p.T, s), "LED loop (box)");
+    } else if (p.w64) {
+        fpmk::BoxArgs bx{};
+        bx.frames = frames;
+        bx.pitch = pitch;
+        bx.frame_stride = pitch * r.height;
+        if (s0 == 0 && s1 == p.num_slots && !acc) {  // whole run: the work queue may serve it
+            a.work = p.work.ensure(size_t(p.T) + 1);
+            a.isum = p.isum.ensure(size_t(p.T) * p.L);
+        }
+        ck(fpmk::launch_loop_w64(r.mode, a, bx, p.T, s), "LED loop (warp per tile)");
     } else {
         const CUtensorMap map = encode_frames_map(frames, p.F, r.height, r.width, pitch);
         if (p.G == 1 && s0 == 0 && s1 == p.num_slots && !acc) {  // whole run: the work queue may serve it
@@ -529,7 +550,8 @@ bool same_request(const HostSlot& c, const fpmgpu_recon_request& r, std::vector<
     ki.insert(ki.end(), r.seq_frame, r.seq_frame + r.num_leds);
     // kernel-selection overrides change the plans too
     const char* cl_env = std::getenv("FPM_B200_CLUSTER");
-    ki.insert(ki.end(), {box_forced() ? 1 : 0, cl_env ? std::atoi(cl_env) : -1});
+    const char* w_env = std::getenv("FPM_B200_W64");
+    ki.insert(ki.end(), {box_forced() ? 1 : 0, cl_env ? std::atoi(cl_env) : -1, w_env && w_env[0] ? w_env[0] : -1});
     kd.push_back(r.alpha);
     kd.push_back(r.beta);
     if (r.tile_defocus_um) kd.insert(kd.end(), r.tile_defocus_um, r.tile_defocus_um + r.num_tiles);

@@ -92,8 +92,9 @@ __device__ __forceinline__ float2 w8_2(float2 a) {
 // In-place 8-point DFT, natural order in and out (radix-2 decimation in
 // frequency, 3 stages). The W8 / W8^3 twiddles of the odd half share the
 // factor 1/sqrt(2), folded into the last stage's FFMA2s. MID4: inputs 0, 1, 6, 7
-// are known zero, so the first butterfly stage degenerates to copies.
-template <bool INV, bool MID4>
+// are known zero, so the first butterfly stage degenerates to copies. OMID:
+// only outputs 2..5 are formed (the others are left undefined).
+template <bool INV, bool MID4, bool OMID = false>
 __device__ __forceinline__ void dft8(float2& x0, float2& x1, float2& x2, float2& x3, float2& x4,
                                      float2& x5, float2& x6, float2& x7) {
     float2 a0, a1, a2, a3, a4, a5, a6, a7;
@@ -117,10 +118,16 @@ __device__ __forceinline__ void dft8(float2& x0, float2& x1, float2& x2, float2&
     const float2 Bv = csub(w8_2<INV>(a7), a7);
     const float2 b5u = cadd(A, Bv), b7u = w8_2<INV>(csub(A, Bv));
     const float s = 0.70710678118654752440f;
-    x0 = cadd(b0, b1); x4 = csub(b0, b1);
-    x2 = cadd(b2, b3); x6 = csub(b2, b3);
-    x1 = cfma(s, b5u, b4); x5 = cfma(-s, b5u, b4);
-    x3 = cfma(s, b7u, b6); x7 = cfma(-s, b7u, b6);
+    x4 = csub(b0, b1);
+    x2 = cadd(b2, b3);
+    x5 = cfma(-s, b5u, b4);
+    x3 = cfma(s, b7u, b6);
+    if (!OMID) {
+        x0 = cadd(b0, b1);
+        x6 = csub(b2, b3);
+        x1 = cfma(s, b5u, b4);
+        x7 = cfma(-s, b7u, b6);
+    }
 }
 
 // 2-D 8x8 DFT over the register block v[a][b]: first along a (for each b),

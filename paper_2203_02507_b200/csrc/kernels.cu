@@ -44,6 +44,12 @@ constexpr int kGroupThreads = 128;
 #ifndef FPM_PASS_UNROLL
 #define FPM_PASS_UNROLL 1  // two specialised FFT bodies (pruning resolved at compile time); 0: one rolled body
 #endif
+#ifndef FPM_PAIR_ROT
+#define FPM_PAIR_ROT 1  // step-1 pair twiddles W8^1, W8^3 as rotations (scale folded into the column twiddles)
+#endif
+#ifndef FPM_MOD_SEL
+#define FPM_MOD_SEL 0  // |e| = 0 rule by selects (1; measured +1.5%) or by a 2^-60 nudge of Re (0)
+#endif
 #ifndef FPM_LOOP_MINB
 #define FPM_LOOP_MINB 4  // resident tiles per SM the register budget is sized for
 #endif
@@ -121,8 +127,8 @@ __device__ __forceinline__ int tswz(int pp) {
 // the prunings resolve at compile time: skip_cols drops the zero columns of the
 // disk-limited input (IFFT), skip_rows the rows the scatter never reads (FFT).
 __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, const float4* W4_s, int p, int h,
-                                                float sg, const float2 (&tw)[4], const float2 (&twsw)[4], int g,
-                                                bool skip_cols, bool skip_rows) {
+                                                float sg, const float2 (&tw)[4], const float2 (&twsw)[4], float kh,
+                                                float c1, float c3, int g, bool skip_cols, bool skip_rows) {
     const int tr = p >> 3, tc = p & 7;
     // step 1: DFT8 over n1r (registers), then the pair DFT over n1c (DIT). Pruned IFFT
     // (skip_cols): only rows a in [2, 6) of columns j in {1, 2} hold data, and the
@@ -140,6 +146,23 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
 #pragma unroll
         for (int a = 0; a < 8; ++a) dft4<false>(v[a][0], v[a][1], v[a][2], v[a][3]);  // E (h = 0) or O (h = 1)
     }
+    // pair DIT: X[m] = E + W8^m O (even lane), X[m + 4] = E - W8^m O (odd lane). m = 2: W8^2 = -i,
+    // a swap and a sign off the FMA pipe. m = 1, 3: W8^m O = s R with s = 1/sqrt(2) and R a
+    // rotation (one FFMA2 on the odd lane instead of a complex multiply): the odd lane forms
+    // E - s R exactly, the even lane +-(sqrt(2) E + R), whose factor +-s rides on its column
+    // twiddle (table entries pre-scaled)
+#if FPM_PAIR_ROT
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        v[a][1] = cfma(kh, make_float2(v[a][1].y, -v[a][1].x), v[a][1]);  // odd: R1 = (x + y, y - x)
+        v[a][2] = mul_mi_odd(v[a][2], h);
+        v[a][3] = cfma(kh, make_float2(-v[a][3].y, v[a][3].x), v[a][3]);  // odd: -R3 = (x - y, x + y)
+        v[a][0] = cfma(sg, v[a][0], shfl_pair(v[a][0]));  // E + O | E - O
+        v[a][1] = cfma(c1, v[a][1], shfl_pair(v[a][1]));  // sqrt(2) E + R1 | E - s R1
+        v[a][2] = cfma(sg, v[a][2], shfl_pair(v[a][2]));
+        v[a][3] = cfma(c3, v[a][3], shfl_pair(v[a][3]));  // -(sqrt(2) E + R3) | E - s R3
+    }
+#else
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
 #pragma unroll
@@ -148,6 +171,7 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
 #pragma unroll
         for (int m = 0; m < 4; ++m) v[a][m] = cfma(sg, v[a][m], shfl_pair(v[a][m]));  // E + O' | E - O'
     }
+#endif
     // twiddle W64^(n0r k0r + n0c k0c), k0 = (a, 4h + m); table entries (w, (-w.y, w.x))
 #pragma unroll
     for (int a = 1; a < 8; ++a) {
@@ -185,10 +209,15 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
         v[n0r][2] = make_float2(q1.x, q1.y);
         v[n0r][3] = make_float2(q1.z, q1.w);
     }
-    // step 2: DFT8 over n0r, then the pair DFT over n0c (DIF)
+    // step 2: DFT8 over n0r, then the pair DFT over n0c (DIF); pruned FFT (skip_rows):
+    // only outputs a in [2, 6) of the DFT8 are formed
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-        dft8<false, false>(v[0][i], v[1][i], v[2][i], v[3][i], v[4][i], v[5][i], v[6][i], v[7][i]);
+    for (int i = 0; i < 4; ++i) {
+        if (skip_rows)
+            dft8<false, false, true>(v[0][i], v[1][i], v[2][i], v[3][i], v[4][i], v[5][i], v[6][i], v[7][i]);
+        else
+            dft8<false, false>(v[0][i], v[1][i], v[2][i], v[3][i], v[4][i], v[5][i], v[6][i], v[7][i]);
+    }
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
         if ((a < 2 || a > 5) && skip_rows) continue;
@@ -284,7 +313,9 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
         const int m = t < 64 ? t : ((((e & 15) >> 1) * (4 * (e & 1) + (e >> 4))) & 63);
         double s, c;
         sincospi(-double(m) / 32.0, &s, &c);
-        W4_s[t] = make_float4(float(c), float(s), -float(s), float(c));
+        // column twiddles of the even lane for m = 1, 3 carry the pair combine's +-1/sqrt(2)
+        const double f = (FPM_PAIR_ROT && t >= 64 && (e & 1) == 0 && ((e >> 4) & 1)) ? ((e >> 4) == 1 ? 1.0 : -1.0) * 0.70710678118654752440 : 1.0;
+        W4_s[t] = make_float4(float(c * f), float(s * f), -float(s * f), float(c * f));
     }
     // pair-combine twiddles W8^m, m = 1..3, on the odd lane (1 on the even lane)
     float2 tw[4];
@@ -299,12 +330,14 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
 #pragma unroll
     for (int m = 0; m < 4; ++m) twsw[m] = make_float2(-tw[m].y, tw[m].x);
     const float sg = h ? -1.f : 1.f;
+    const float kh = h ? 1.f : 0.f;  // step-1 rotations on the odd lane only
+    const float c1 = h ? -0.70710678118654752440f : 1.41421356237309504880f;
+    const float c3 = h ? 0.70710678118654752440f : -1.41421356237309504880f;
     if (MEAS == kMeasTMA && tl == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const float sgn = ((tr + tc) & 1) ? -1.f : 1.f;  // checkerboard (-1)^(i+j), constant per thread
-    const float sgn_eps = sgn * 0x1p-60f;            // see the modulus replacement
     const float inv_n2 = 1.0f / 4096.0f;  // ifft2's 1/(rows*cols) (field.cpp:64-66)
     uint32_t phase = 0;
     // canvas offset of lattice position (a, j) relative to the sub-aperture origin
@@ -434,7 +467,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
 #pragma unroll 1
 #endif
             for (int pass = 0; pass < 2; ++pass) {
-            fft64x64_fwd_rt(v, T_s, W4_s, p, h, sg, tw, twsw, g, PRUNE && pass == 0, PRUNE && pass == 1);
+            fft64x64_fwd_rt(v, T_s, W4_s, p, h, sg, tw, twsw, kh, c1, c3, g, PRUNE && pass == 0, PRUNE && pass == 1);
             if (pass == 1) break;
 
             // ---- modulus replacement with sqrt(I) and residual sums (recon.cpp:115-124):
@@ -463,17 +496,29 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
                         Iv = args.meas_f32[(tr + 8 * a) * 64 + tc + 8 * b];
                         if (first) den_f += Iv;
                     }
-                    // branch-free |e| = 0 rule (recon.cpp:122): nudging Re by sgn 2^-60 leaves every
-                    // value with |Re| >= 2^-35 bit-identical and maps e = 0 to (sgn 2^-60, 0), whose
-                    // replacement is exactly the checkerboarded sqrt(I) + 0i
+                    // |e| = 0 rule (recon.cpp:122): e' = sqrt(I) + 0i, checkerboarded (sgn), by two
+                    // selects on the ALU pipe
                     const float meas = sqrt_ftz(Iv);
+#if FPM_MOD_SEL
                     const float2 uu = v[a][u];
-                    const float ux = uu.x + sgn_eps;
+                    const float m2 = fmaf(uu.x, uu.x, uu.y * uu.y);
+                    const bool zero = m2 == 0.f;
+                    const float r = rsqrt_ftz(fmaxf(m2, kTiny));
+                    const float dm = fmaf(m2 * r, inv_n2, -meas);  // |e| - sqrt(I)
+                    num = fmaf(dm, dm, num);
+                    const float sc = zero ? meas : meas * r;
+                    const float ux = zero ? sgn : uu.x;
+#else
+                    // nudging Re by sgn 2^-60 leaves every value with |Re| >= 2^-35 bit-identical
+                    // and maps e = 0 to (sgn 2^-60, 0), whose replacement is sqrt(I) + 0i, signed
+                    const float2 uu = v[a][u];
+                    const float ux = uu.x + sgn * 0x1p-60f;
                     const float m2 = fmaf(ux, ux, uu.y * uu.y);
                     const float r = rsqrt_ftz(fmaxf(m2, kTiny));
                     const float dm = fmaf(m2 * r, inv_n2, -meas);  // |e| - sqrt(I)
                     num = fmaf(dm, dm, num);
                     const float sc = meas * r;
+#endif
                     // uu = conj(e n^2): undo the conjugation
                     v[a][u] = make_float2(ux * sc, -uu.y * sc);
                 }

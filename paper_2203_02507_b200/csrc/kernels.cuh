@@ -70,6 +70,11 @@ cudaError_t launch_loop_cluster(int n, int mode, int cl, const LoopArgs& a, cons
 
 size_t loop_smem_bytes(int G, int nslots, int L, int iters);
 
+// n = 64, one warp per tile (kernels_w64.cu): sequential schedules whose pupil
+// disk lies in rows/cols [16, 48) of the block.
+size_t loop_w64_smem_bytes(int L, int iters);
+cudaError_t launch_loop_w64(int mode, const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s);
+
 #ifdef __CUDACC__
 // Per-pass mean residuals of the stages a launch touched (all of them for a
 // whole run; a stage range for the online passes, accumulated).
