@@ -25,6 +25,9 @@
 // single-tile runs, where one CTA would leave 147 SMs idle (BASELINE config 2).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "warp_fft.cuh"
 
@@ -46,6 +49,7 @@ size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
     b += size_t(iters) * sizeof(double) + 2 * sizeof(uint64_t);
     b += nbuf * size_t(nw) * 4 * sizeof(float) + 4 * sizeof(float);
     b += size_t(L) * (sizeof(short2) + sizeof(int) + 1) + 16;
+    b += 8;  // work-queue item
     return b;
 }
 
@@ -114,7 +118,6 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     constexpr bool DB = NLR <= 128;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = int(cluster.block_rank());
-    const int tile = blockIdx.x / CL;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int L = args.L, B = bx.box, b0 = bx.b0;
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -149,17 +152,12 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     int* F_s = reinterpret_cast<int*>(sp);
     sp += size_t(L) * sizeof(int);
     uint8_t* B_s = sp;
+    sp += size_t(L);
+    sp = smem_raw + ((sp - smem_raw + 3) & ~3);
+    int* item_s = reinterpret_cast<int*>(sp);  // work queue: the cluster's current item (rank 0's copy)
 
-    float2* canvas = args.canvas + size_t(tile) * NC * NC;
-    float2* pupil = args.pupils + size_t(tile) * NLR * NLR;
-    const int2 txy = args.tile_xy[tile];
     for (int k = threadIdx.x; k < NLR; k += NT) SR[k] = bx.sup_rows[k];
-    for (int k = threadIdx.x; k < L; k += NT) {
-        O_s[k] = args.origins[size_t(tile) * L + k];
-        F_s[k] = args.seq_frame[k];
-        B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
-    }
-    for (int k = threadIdx.x; k < args.iters; k += NT) stage_sum[k] = 0.0;
+    for (int k = threadIdx.x; k < L; k += NT) F_s[k] = args.seq_frame[k];
     WarpFFT<M> F;
     F.init(l, NLR);
     const float inv_n2 = 1.0f / float(NLR * NLR);
@@ -170,10 +168,61 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     }
     cluster.sync();  // every CTA of the cluster is resident before any DSMEM access
 
+    // work queue (sequential whole runs, more tiles than resident clusters): items
+    // j = it * T + tile, claimed by rank 0 and read by every CTA through DSMEM; item j
+    // depends on item j - T (the tile's previous pass), claimed 3.5 rounds earlier at
+    // BASELINE config 5. Every update runs the same instructions as in the
+    // one-cluster-per-tile launch: bit-identical
+    const bool queue = args.work != nullptr;
+    const int n_items = args.T * args.iters;
+    int par = 0;
+    uint32_t nupd = 0;  // updates run by this CTA (mbarrier phase of buffer `par` = (nupd >> 1) & 1)
+    for (int round = 0;; ++round) {
+    int tile, it_q = 0;
+    if (queue) {
+        if (rank == 0 && threadIdx.x == 0) {
+            if (round > 0) {  // release: the previous item's canvas/pupil writes (cluster barrier below)
+                const int jp = *item_s;
+                __threadfence();
+                asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(args.work + 1 + jp % args.T), "r"(jp / args.T + 1)
+                             : "memory");
+            }
+            const int j = atomicAdd(args.work, 1);
+            if (j < n_items && j >= args.T) {  // acquire: the tile's previous pass is complete
+                const int* flag = args.work + 1 + (j % args.T);
+                int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                    if (v < j / args.T) __nanosleep(256);
+                } while (v < j / args.T);
+            }
+            *item_s = j;
+        }
+        cluster.sync();
+        const int j = *cluster.map_shared_rank(item_s, 0);
+        if (threadIdx.x == 0) __threadfence();
+        cluster.sync();  // every CTA has read the item before rank 0 claims the next
+        if (j >= n_items) break;
+        tile = j % args.T;
+        it_q = j / args.T;
+    } else {
+        if (round > 0) break;
+        tile = blockIdx.x / CL;
+    }
+    float2* canvas = args.canvas + size_t(tile) * NC * NC;
+    float2* pupil = args.pupils + size_t(tile) * NLR * NLR;
+    const int2 txy = args.tile_xy[tile];
+    for (int k = threadIdx.x; k < L; k += NT) {
+        O_s[k] = args.origins[size_t(tile) * L + k];
+        B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
+    }
+    for (int k = threadIdx.x; k < args.iters; k += NT) stage_sum[k] = 0.0;
+    __syncthreads();
+
     // schedule entries: sequential slot e = (e / L, e % L); pipelined slots hold two
     // entries each (stage < 0 = idle), run back to back
     const int G = args.slots ? 2 : 1;
-    const int e_end = args.num_slots * G;
+    const int e_end = queue ? (it_q + 1) * L : args.num_slots * G;
     auto entry_at = [&](int e, int& it, int& pos) -> bool {
         if (G == 1) {
             it = e / L;
@@ -211,14 +260,12 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
             }
         }
     };
-    int e = next_entry(args.slot_begin * G - 1);
+    int e = next_entry((queue ? it_q * L : args.slot_begin * G) - 1);
     if (e >= 0) {
         int it0, pos0;
         entry_at(e, it0, pos0);
         stage(pos0);
     }
-    int par = 0;
-    uint32_t nupd = 0;  // updates run by this launch (mbarrier phase of buffer `par` = (nupd >> 1) & 1)
     for (; e >= 0;) {
         int it, pos;
         entry_at(e, it, pos);
@@ -448,8 +495,16 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
         ++nupd;
         e = e_next;
     }
-    if (DB) cluster.sync();  // no CTA leaves while another still reads its slab
-    if (rank == 0) store_residuals(args, tile, stage_sum, G == 1);
+    if (DB) cluster.sync();  // no CTA leaves (or moves to the next item) while another still reads its slab
+    if (rank == 0) {
+        if (queue) {
+            if (threadIdx.x == 0) args.residuals[size_t(tile) * args.iters + it_q] = stage_sum[it_q] / double(L);
+        } else {
+            store_residuals(args, tile, stage_sum, G == 1);
+        }
+    }
+    if (queue) cluster.sync();  // the item's canvas and pupil writes precede rank 0's release
+    }  // items
 }
 
 template <int NLR, int MODE, int NC, int CL, int NW>
@@ -462,8 +517,37 @@ cudaError_t launch_cluster_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStr
         e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
+    LoopArgs a2 = a;
+    int clusters = T;
+    {
+        const char* qe = std::getenv("FPM_B200_QUEUE");
+        const int q = qe && qe[0] ? (qe[0] == '1' ? 1 : 0) : -1;
+        a2.work = nullptr;
+        if (a.work && !a.slots && a.slot_begin == 0 && a.num_slots == a.iters * a.L && q != 0) {
+            // resident clusters: the occupancy calculator for this cluster shape
+            cudaLaunchConfig_t oc{};
+            oc.gridDim = dim3(unsigned(T * CL));
+            oc.blockDim = dim3(NW * 32);
+            oc.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = CL;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            oc.attrs = at;
+            oc.numAttrs = 1;
+            int resident = 0;
+            if ((e = cudaOccupancyMaxActiveClusters(&resident, k, &oc)) != cudaSuccess) return e;
+            resident = std::max(resident, 1);
+            if (T > resident || q == 1) {
+                a2.work = a.work;
+                clusters = q == 1 ? std::min(resident, T * a.iters) : resident;
+                if ((e = cudaMemsetAsync(a.work, 0, sizeof(int) * size_t(T + 1), s)) != cudaSuccess) return e;
+            }
+        }
+    }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(T * CL));
+    cfg.gridDim = dim3(unsigned(clusters * CL));
     cfg.blockDim = dim3(NW * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -474,7 +558,7 @@ cudaError_t launch_cluster_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStr
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, a, b);
+    return cudaLaunchKernelEx(&cfg, k, a2, b);
 }
 
 }  // namespace

@@ -395,6 +395,30 @@ def test_work_queue_bit_identical(eng, monkeypatch, mode, parts):
             assert np.array_equal(pa, pb)
 
 
+@pytest.mark.parametrize("n,mode", [(256, "epry"), (128, "gs")])
+def test_cluster_work_queue_bit_identical(eng, monkeypatch, n, mode):
+    """The cluster kernel as a persistent work queue over (pass, tile) items
+    (FPM_B200_QUEUE=1: a grid of clusters wider than the tile count, most items
+    waiting on their tile's previous pass) gives one cluster per tile's bits."""
+    cfg = fpm.OpticalConfig(tile_size=n, tile_overlap=0, upsample=4, led_scan_rows=5, led_scan_cols=5)
+    fs, _, seq, _ = dataset(cfg, fov=2 * n, seed=42, defocus_um=4.0)
+    specs = fpm.partition_tiles(fs.width(), fs.height(), cfg)
+    opt = fpm.RunOptions(iters=3, mode=mode, tile_defocus_um=[2.0, -3.0, 0.0, 4.0][: len(specs)])
+    monkeypatch.setenv("FPM_B200_BANDS", "1")
+    monkeypatch.setenv("FPM_B200_CLUSTER", "4")
+    monkeypatch.setenv("FPM_B200_QUEUE", "0")
+    a = fpm.run_offline(fs, cfg, seq, opt, engine=fpm.Engine(0), stitch=False)
+    monkeypatch.setenv("FPM_B200_QUEUE", "1")
+    b = fpm.run_offline(fs, cfg, seq, opt, engine=fpm.Engine(0), stitch=False)
+    assert len(specs) == 4
+    assert np.array_equal(a.tiles, b.tiles)
+    assert np.array_equal(np.array([m.pass_mean_residual for m in a.tile_metrics]),
+                          np.array([m.pass_mean_residual for m in b.tile_metrics]))
+    if mode == "epry":
+        for pa, pb in zip(a.pupils, b.pupils):
+            assert np.array_equal(pa, pb)
+
+
 @pytest.mark.parametrize("n,cl,mode", [(128, 2, "epry"), (128, 4, "gs"), (128, 8, "epry"), (128, 16, "gs"), (256, 2, "gs"),
                                        (256, 4, "epry"), (256, 8, "gs")])
 def test_cluster_kernel_matches_box_kernel(eng, monkeypatch, n, cl, mode):
