@@ -417,8 +417,10 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
             tma_load_crop(I_s, &tmap, bar, txy.x, txy.y, F_s[e.y]);
         }
     };
+    // sequential slots (G == 1): (iteration, position) by counters, not a division per slot
+    int c_it = G == 1 ? s_begin / L : 0, c_pos = G == 1 ? s_begin - c_it * L : 0;
     for (int s = s_begin; s < s_end; ++s) {
-        const int2 e = slot_entry<G>(args, s, g);
+        const int2 e = G == 1 ? make_int2(c_it, c_pos) : slot_entry<G>(args, s, g);
         if (e.x >= 0) {
             if (!issued) issue(e);
             issued = false;
@@ -537,7 +539,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
 
             // prefetch the measurement of this group's next update
             if (s + 1 < s_end) {
-                const int2 nx = slot_entry<G>(args, s + 1, g);
+                const int2 nx = G == 1 ? (c_pos + 1 == L ? make_int2(c_it + 1, 0) : make_int2(c_it, c_pos + 1))
+                                       : slot_entry<G>(args, s + 1, g);
                 if (nx.x >= 0) {
                     issue(nx);
                     issued = true;
@@ -575,7 +578,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
                 for (int c0 = 0; c0 < NP; c0 += 8) {
                     float2 Ov[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) Ov[q] = cv[Lat::a(c0 + q) * 8 * N + 16 * Lat::j(c0 + q)];
+                    for (int q = 0; q < 8; ++q)
+                        Ov[q] = cv[Lat::a(c0 + q) * 8 * N + 16 * Lat::j(c0 + q)];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const int qq = c0 + q;
@@ -593,6 +597,10 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
             }
         }
         __syncthreads();  // slot barrier: canvas writes visible to the next update's gather
+        if (G == 1 && ++c_pos == L) {
+            c_pos = 0;
+            ++c_it;
+        }
     }
 
     // ---- per-pass mean residual; EPRY pupil back to global
