@@ -47,6 +47,9 @@ constexpr int kGroupThreads = 128;
 #ifndef FPM_PAIR_ROT
 #define FPM_PAIR_ROT 1  // step-1 pair twiddles W8^1, W8^3 as rotations (scale folded into the column twiddles)
 #endif
+#ifndef FPM_O_STAGE
+#define FPM_O_STAGE 1  // EPRY scatter: old canvas values staged by cp.async into the measurement buffer
+#endif
 #ifndef FPM_MOD_SEL
 #define FPM_MOD_SEL 0  // |e| = 0 rule by selects (1; measured +1.5%) or by a 2^-60 nudge of Re (0)
 #endif
@@ -413,6 +416,9 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
     bool pupil_dirty = true;  // EPRY: max|P|^2 changes only after a pupil step
     auto issue = [&](int2 e) {
         if (MEAS == kMeasTMA && tl == 0) {
+            // the staging buffer's earlier generic-proxy accesses (modulus reads, the EPRY
+            // canvas staging) are ordered before the TMA's async-proxy write
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar, kIBytes);
             tma_load_crop(I_s, &tmap, bar, txy.x, txy.y, F_s[e.y]);
         }
@@ -537,8 +543,21 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
             }
             group_sync(g);  // staging and transpose buffers free; reductions visible
 
+            // EPRY (pruned, sequential): the scatter's old canvas values go into the now-free
+            // measurement staging buffer by cp.async, their latency under pass 1; the next
+            // crop's TMA is then issued at the top of the next update
+            constexpr bool kOStage = FPM_O_STAGE && MODE == kModeEPRY && PRUNE && G == 1 && MEAS == kMeasTMA;
+            if constexpr (kOStage) {
+                float2* Ostg = reinterpret_cast<float2*>(I_s);
+#pragma unroll
+                for (int q = 0; q < NP; ++q)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Ostg + q * kGroupThreads + tl)),
+                                 "l"(cv + Lat::a(q) * 8 * N + 16 * Lat::j(q))
+                                 : "memory");
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
             // prefetch the measurement of this group's next update
-            if (s + 1 < s_end) {
+            if (!kOStage && s + 1 < s_end) {
                 const int2 nx = G == 1 ? (c_pos + 1 == L ? make_int2(c_it + 1, 0) : make_int2(c_it, c_pos + 1))
                                        : slot_entry<G>(args, s + 1, g);
                 if (nx.x >= 0) {
@@ -574,12 +593,18 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
             } else {
                 const bool upd_o = inv_pmax > 0.f, upd_p = inv_omax > 0.f;
                 pupil_dirty = upd_p;
+                if constexpr (FPM_O_STAGE && MODE == kModeEPRY && PRUNE && G == 1 && MEAS == kMeasTMA)
+                    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own slots
 #pragma unroll
                 for (int c0 = 0; c0 < NP; c0 += 8) {
                     float2 Ov[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        Ov[q] = cv[Lat::a(c0 + q) * 8 * N + 16 * Lat::j(c0 + q)];
+                    for (int q = 0; q < 8; ++q) {
+                        if constexpr (FPM_O_STAGE && MODE == kModeEPRY && PRUNE && G == 1 && MEAS == kMeasTMA)
+                            Ov[q] = reinterpret_cast<const float2*>(I_s)[(c0 + q) * kGroupThreads + tl];
+                        else
+                            Ov[q] = cv[Lat::a(c0 + q) * 8 * N + 16 * Lat::j(c0 + q)];
+                    }
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const int qq = c0 + q;
