@@ -39,6 +39,16 @@ namespace cg = cooperative_groups;
 
 namespace fpmk {
 
+#ifndef FPM_CL_STAGE
+#define FPM_CL_STAGE 1  // n = 256: phase-A canvas/pupil box rows staged one row ahead by cp.async (per warp)
+#endif
+
+// n = 256 phase-A row staging: per warp one box row of canvas and pupil, box
+// columns rounded up to 8 (the XOR swizzle below stays inside)
+__host__ __device__ static size_t row_stage_bytes(int n, int box, int nw) {
+    return (FPM_CL_STAGE && n == 256) ? size_t(nw) * 2 * size_t((box + 7) & ~7) * sizeof(float2) : 0;
+}
+
 size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
     const size_t sw = size_t(n / cl);
     const size_t nbuf = n <= 128 ? 2 : 1;                  // double-buffered slabs (small n)
@@ -46,6 +56,7 @@ size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
     b += sw * size_t(n) * sizeof(uint16_t);               // measurement slab
     b += size_t(n) * sizeof(short2);                      // support run per row
     b = (b + 15) & ~size_t(15);
+    b += row_stage_bytes(n, box, nw);                     // phase-A row staging (n = 256)
     b += size_t(iters) * sizeof(double) + 2 * sizeof(uint64_t);
     b += nbuf * size_t(nw) * 4 * sizeof(float) + 4 * sizeof(float);
     b += size_t(L) * (sizeof(short2) + sizeof(int) + 1) + 16;
@@ -57,6 +68,12 @@ namespace {
 
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                      static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
                  "l"(gsrc)
                  : "memory");
@@ -103,7 +120,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int NLR, int MODE, int NC, int CL, int NW>
-__global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cluster(const LoopArgs args, const BoxArgs bx) {
+__global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32)) fpm_loop_cluster(const LoopArgs args, const BoxArgs bx) {
     constexpr int M = NLR / 32;
     constexpr int SW = NLR / CL;  // columns per CTA
     constexpr int RS = SW + 1;    // slab row stride (float2): column reads conflict-free
@@ -134,6 +151,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
     short2* SR = reinterpret_cast<short2*>(sp);  // support run [x, y) of each row
     sp += size_t(NLR) * sizeof(short2);
     sp = smem_raw + ((sp - smem_raw + 15) & ~15);
+    constexpr bool STG = FPM_CL_STAGE && NLR == 256;
+    const int RBW = (B + 7) & ~7;  // staged row width (box columns, XOR-swizzled in groups of 8)
+    float2* RB = reinterpret_cast<float2*>(sp) + size_t(w) * 2 * RBW;  // this warp's [canvas | pupil] row
+    sp += row_stage_bytes(NLR, B, NW);
     double* stage_sum = reinterpret_cast<double*>(sp);
     sp += size_t(args.iters) * sizeof(double);
     uint64_t* mbA = reinterpret_cast<uint64_t*>(sp);  // DB: phase-A slab arrivals, one per parity
@@ -296,8 +317,20 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
                 Pa[k0] = on ? pupil[ii * NLR + c] : make_float2(0.f, 0.f);
             }
         };
+        // n = 256: the warp's next box row (canvas and pupil over the box columns) is staged
+        // into its row buffer by cp.async while the current row transforms; slot x ^ ((x >> 3) & 7)
+        // makes the gather's stride-8 reads conflict-free
+        auto rb_slot = [](int x) { return x ^ ((x >> 3) & 7); };
+        auto stage_row = [&](int ii) {
+            for (int xx = l; xx < B; xx += 32) {
+                cp_async8(RB + rb_slot(xx), cv + size_t(ii) * NC + b0 + xx);
+                cp_async8(RB + RBW + rb_slot(xx), pupil + ii * NLR + b0 + xx);
+            }
+            cp_async_commit();
+        };
         const int i0 = rfirst + CL * w;
         if (PF && i0 < b0 + B) load_row(i0);
+        if (STG && i0 < b0 + B) stage_row(i0);
         for (int i = i0; i < b0 + B; i += CL * NW) {
             float2 x[M];
             if constexpr (PF) {
@@ -312,6 +345,28 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 0) fpm_loop_cl
                     }
                 }
                 if (i + CL * NW < b0 + B) load_row(i + CL * NW);
+            } else if constexpr (STG) {
+                cp_async_wait_all();
+                __syncwarp();
+                const short2 run = SR[i];
+#pragma unroll
+                for (int k0 = 0; k0 < M; ++k0) {
+                    const int c = k0 + M * brev5(l);
+                    float2 v = make_float2(0.f, 0.f);
+                    if (c >= run.x && c < run.y) {
+                        const float2 O = RB[rb_slot(c - b0)];
+                        const float2 P = RB[RBW + rb_slot(c - b0)];
+                        const float2 g = cmul(O, P);
+                        v = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
+                        if (MODE == kModeEPRY) {
+                            omax = fmaxf(omax, cabs2(O));
+                            pmax = fmaxf(pmax, cabs2(P));
+                        }
+                    }
+                    x[k0] = v;
+                }
+                __syncwarp();  // every lane has read the buffer
+                if (i + CL * NW < b0 + B) stage_row(i + CL * NW);
             } else {
                 const short2 run = SR[i];
 #pragma unroll
