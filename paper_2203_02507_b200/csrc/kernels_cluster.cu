@@ -39,6 +39,9 @@ namespace cg = cooperative_groups;
 
 namespace fpmk {
 
+#ifndef FPM_CL_STAGE_C
+#define FPM_CL_STAGE_C 1  // n = 256: phase-C scatter operands staged the same way, under the row's FFT
+#endif
 #ifndef FPM_CL_STAGE
 #define FPM_CL_STAGE 1  // n = 256: phase-A canvas/pupil box rows staged one row ahead by cp.async (per warp)
 #endif
@@ -510,6 +513,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                     Oc[k0] = (MODE == kModeEPRY && on) ? cv[size_t(i) * NC + c] : make_float2(0.f, 0.f);
                 }
             }
+            if constexpr (STG && FPM_CL_STAGE_C) stage_row(i);  // the row's canvas and pupil, under its FFT
             float2 x[M];
 #pragma unroll
             for (int m = 0; m < M; ++m) {
@@ -517,6 +521,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 x[m] = cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)];
             }
             F.f1(x);
+            if constexpr (STG && FPM_CL_STAGE_C) {
+                cp_async_wait_all();
+                __syncwarp();
+            }
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int c = k0 + M * brev5(l);
@@ -525,17 +533,22 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 float2* dst = cv + size_t(i) * NC + c;
                 float2* pp = pupil + i * NLR + c;
                 float2 P;
-                if constexpr (PFC) P = Pc[k0]; else P = *pp;
+                if constexpr (PFC) P = Pc[k0];
+                else if constexpr (STG && FPM_CL_STAGE_C) P = RB[RBW + rb_slot(c - b0)];
+                else P = *pp;
                 if (MODE == kModeGS) {
                     *dst = cmulc(psi2, P);
                 } else {
                     float2 O;
-                    if constexpr (PFC) O = Oc[k0]; else O = *dst;
+                    if constexpr (PFC) O = Oc[k0];
+                    else if constexpr (STG && FPM_CL_STAGE_C) O = RB[rb_slot(c - b0)];
+                    else O = *dst;
                     const float2 d = csub(psi2, cmul(O, P));
                     if (inv_pmax > 0.f) *dst = cadd(O, cscale(cmulc(d, P), inv_pmax));
                     if (inv_omax > 0.f) *pp = cadd(P, cscale(cmulc(d, O), inv_omax));
                 }
             }
+            if constexpr (STG && FPM_CL_STAGE_C) __syncwarp();  // the buffer is read before the next row's staging
         }
         // slabs reusable. Only a pupil step (bright-field EPRY) leaves writes another CTA
         // reads next (pupil rows follow the moving box rows): then release; else a relaxed
