@@ -46,10 +46,10 @@ namespace fpmk {
 #define FPM_CL_STAGE 1  // n = 256: phase-A canvas/pupil box rows staged one row ahead by cp.async (per warp)
 #endif
 
-// n = 256 phase-A row staging: per warp one box row of canvas and pupil, box
-// columns rounded up to 8 (the XOR swizzle below stays inside)
+// n = 256 row staging: per warp one box row of canvas and pupil, box columns
+// rounded up to 16 (the XOR swizzle below stays inside each group of 16)
 __host__ __device__ static size_t row_stage_bytes(int n, int box, int nw) {
-    return (FPM_CL_STAGE && n == 256) ? size_t(nw) * 2 * size_t((box + 7) & ~7) * sizeof(float2) : 0;
+    return (FPM_CL_STAGE && n == 256) ? size_t(nw) * 2 * size_t((box + 15) & ~15) * sizeof(float2) : 0;
 }
 
 size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
     sp += size_t(NLR) * sizeof(short2);
     sp = smem_raw + ((sp - smem_raw + 15) & ~15);
     constexpr bool STG = FPM_CL_STAGE && NLR == 256;
-    const int RBW = (B + 7) & ~7;  // staged row width (box columns, XOR-swizzled in groups of 8)
+    const int RBW = (B + 15) & ~15;  // staged row width (box columns, XOR-swizzled in groups of 16)
     float2* RB = reinterpret_cast<float2*>(sp) + size_t(w) * 2 * RBW;  // this warp's [canvas | pupil] row
     sp += row_stage_bytes(NLR, B, NW);
     double* stage_sum = reinterpret_cast<double*>(sp);
@@ -321,9 +321,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             }
         };
         // n = 256: the warp's next box row (canvas and pupil over the box columns) is staged
-        // into its row buffer by cp.async while the current row transforms; slot x ^ ((x >> 3) & 7)
-        // makes the gather's stride-8 reads conflict-free
-        auto rb_slot = [](int x) { return x ^ ((x >> 3) & 7); };
+        // into its row buffer by cp.async while the current row transforms; slot x ^ ((x >> 4) & 15)
+        // makes the gather's stride-8 reads conflict-free (a half-warp's stride-16 columns land
+        // in 16 distinct bank pairs)
+        auto rb_slot = [](int x) { return x ^ ((x >> 4) & 15); };
         auto stage_row = [&](int ii) {
             for (int xx = l; xx < B; xx += 32) {
                 cp_async8(RB + rb_slot(xx), cv + size_t(ii) * NC + b0 + xx);
