@@ -144,6 +144,28 @@ __global__ void __launch_bounds__(512) lines_fft_w256(const LinesArgs a) {
     const size_t base = size_t(tile) * NL * NL;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     auto pad = [](int i) { return i + (i >> 5); };
+    // init rows: sqrt of the seed-crop rows this block's 16 output rows interpolate
+    // from, once per crop pixel instead of four times per output pixel
+    constexpr int kSq = 1280;
+    __shared__ float sq[WHICH == 0 ? kSq : 1];
+    int sq_r0 = 0;
+    bool sq_on = false;
+    if (WHICH == 0) {
+        const int n = a.n;
+        const int ya0 = max(int(floorf((l0 + 0.5f) / a.up - 0.5f)), 0);
+        const int yb1 = min(int(floorf((l0 + LPB - 1 + 0.5f) / a.up - 0.5f)) + 1, n - 1);
+        sq_r0 = ya0;
+        sq_on = (yb1 - ya0 + 1) * n <= kSq;
+        if (sq_on) {
+            const int2 txy = a.tile_xy[tile];
+            const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
+            for (int k = threadIdx.x; k < (yb1 - ya0 + 1) * n; k += blockDim.x) {
+                const int r = k / n, c = k - r * n;
+                sq[k] = sqrtf(float(f[size_t(ya0 + r) * a.pitch + c]));
+            }
+        }
+        __syncthreads();
+    }
 
     for (int idx = threadIdx.x; idx < LPB * NL; idx += blockDim.x) {
         int line, e;
@@ -164,12 +186,22 @@ __global__ void __launch_bounds__(512) lines_fft_w256(const LinesArgs a) {
             const int yb = min(ya + 1, n - 1), xb = min(xa + 1, n - 1);
             ya = max(ya, 0);
             xa = max(xa, 0);
-            const int2 txy = a.tile_xy[tile];
-            const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
-            const float v00 = sqrtf(float(f[size_t(ya) * a.pitch + xa]));
-            const float v01 = sqrtf(float(f[size_t(ya) * a.pitch + xb]));
-            const float v10 = sqrtf(float(f[size_t(yb) * a.pitch + xa]));
-            const float v11 = sqrtf(float(f[size_t(yb) * a.pitch + xb]));
+            float v00, v01, v10, v11;
+            if (sq_on) {
+                const float* q0 = sq + (ya - sq_r0) * n;
+                const float* q1 = sq + (yb - sq_r0) * n;
+                v00 = q0[xa];
+                v01 = q0[xb];
+                v10 = q1[xa];
+                v11 = q1[xb];
+            } else {
+                const int2 txy = a.tile_xy[tile];
+                const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
+                v00 = sqrtf(float(f[size_t(ya) * a.pitch + xa]));
+                v01 = sqrtf(float(f[size_t(ya) * a.pitch + xb]));
+                v10 = sqrtf(float(f[size_t(yb) * a.pitch + xa]));
+                v11 = sqrtf(float(f[size_t(yb) * a.pitch + xb]));
+            }
             const float val = (1.f - wy) * ((1.f - wx) * v00 + wx * v01) + wy * ((1.f - wx) * v10 + wx * v11);
             x = make_float2(((i + j) & 1) ? -val : val, 0.f);
         } else if (COLS) {
