@@ -174,7 +174,10 @@ int cluster_choice(int n, int N, int T) {
                               ", cluster " + std::to_string(c));
         return c;
     }
-    if (n == 256 && N == 1024) return 4;
+    // n = 256: 4-CTA clusters (2 per SM); batches small enough for 8-CTA clusters
+    // to be resident at once (a strong-scaled rank of config 5: 32 tiles) take 8
+    // (tools/strong_probe.py: 106 vs 131 ms for 32 tiles)
+    if (n == 256 && N == 1024) return T <= 48 ? 8 : 4;
     if (n == 128 && N == 512 && T * 16 <= 148) return 16;  // single-tile latency (config 2)
     if (n == 128 && N == 512 && T * 8 <= 148) return 8;
     return 0;
