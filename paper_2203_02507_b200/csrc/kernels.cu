@@ -266,8 +266,11 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
     return b;
 }
 
-template <int MODE, bool PRUNE, int MEAS, int G, int N>
-__global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? FPM_LOOP_MINB : 2)
+// MINB: resident tiles per SM the register budget is sized for (4: 128 registers,
+// the throughput build; 2: 255 registers, lower latency per update for batches
+// that leave SMs with at most a few tiles)
+template <int MODE, bool PRUNE, int MEAS, int G, int N, int MINB>
+__global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     fpm_loop64(const __grid_constant__ CUtensorMap tmap, const LoopArgs args) {
     using Lat = Lattice<PRUNE>;
     constexpr int NP = Lat::NP;
@@ -654,10 +657,10 @@ static int queue_override() {
     return e && e[0] ? (e[0] == '1' ? 1 : 0) : -1;
 }
 
-template <int MODE, bool PRUNE, int MEAS, int G, int N>
+template <int MODE, bool PRUNE, int MEAS, int G, int N, int MINB>
 static cudaError_t launch_loop_t(const CUtensorMap* tmap, const LoopArgs& a0, int T, cudaStream_t s) {
     const size_t smem = loop_smem_bytes(G, a0.nslots, a0.L, a0.iters);
-    auto k = fpm_loop64<MODE, PRUNE, MEAS, G, N>;
+    auto k = fpm_loop64<MODE, PRUNE, MEAS, G, N, MINB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     LoopArgs a = a0;
@@ -696,11 +699,27 @@ static cudaError_t launch_loop_t(const CUtensorMap* tmap, const LoopArgs& a0, in
     return cudaGetLastError();
 }
 
+// Register budget by batch: with at most 4 tiles per SM to share (T <= 4 x SMs),
+// the 255-register build's shorter update latency wins (config 3 sharded over 8
+// GPUs, 128 tiles: 10.6 -> 9.0 ms; 512 tiles: 20.8 -> 19.1 ms); a full FOV needs
+// the 4-tiles-per-SM build (1,024 tiles: 33.2 vs 38.0 ms). FPM_B200_MINB=2|4 forces.
+static int loop_minb(int G, int T) {
+    if (G != 1) return 4;
+    if (const char* e = std::getenv("FPM_B200_MINB"); e && e[0]) return e[0] == '2' ? 2 : 4;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return T <= 4 * sms ? 2 : 4;
+}
+
 cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorMap* tmap, const LoopArgs& a, int T,
                           cudaStream_t s) {
-#define FPM_LOOP_CASE(M, P, ME, GG, NN)                                \
-    if (mode == M && prune == P && meas == ME && G == GG && a.N == NN) \
-        return launch_loop_t<M, P, ME, GG, NN>(tmap, a, T, s);
+    const int minb = meas == kMeasTMA ? loop_minb(G, T) : 4;
+#define FPM_LOOP_CASE(M, P, ME, GG, NN)                                                        \
+    if (mode == M && prune == P && meas == ME && G == GG && a.N == NN) {                       \
+        if (GG == 1 && ME == kMeasTMA && P && minb == 2)                                       \
+            return launch_loop_t<M, P, ME, GG, NN, (GG == 1 && ME == kMeasTMA && P) ? 2 : 4>(tmap, a, T, s); \
+        return launch_loop_t<M, P, ME, GG, NN, FPM_LOOP_MINB>(tmap, a, T, s);                    \
+    }
 #define FPM_LOOP_N(M, P, ME, GG) \
     FPM_LOOP_CASE(M, P, ME, GG, 256) FPM_LOOP_CASE(M, P, ME, GG, 512) FPM_LOOP_CASE(M, P, ME, GG, 1024)
     FPM_LOOP_N(kModeGS, true, kMeasTMA, 1)
