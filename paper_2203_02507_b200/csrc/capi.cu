@@ -251,6 +251,7 @@ struct fpmgpu_plan {
     int cl = 0;            // > 0: each tile split over a cluster of cl CTAs (kernels_cluster.cu)
     int box = 0, b0 = 0;
     int support_px = 0;
+    int batch_tiles = 0;  // tiles sharing the GPU with this plan's launch (banded host path); 0 = T
     double radius = 0.0;
     DevBuf<float2> canvas, pupils, pupils_init, scratch;
     DevBuf<uint8_t> support;
@@ -470,6 +471,7 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
     a.nslots = p.nslots;
     a.alpha = float(r.alpha);
     a.beta = float(r.beta);
+    a.batch_T = p.batch_tiles > 0 ? p.batch_tiles : p.T;
     if (p.use_box || p.cl) {
         fpmk::BoxArgs bx{};
         bx.scratch = p.scratch.p;
@@ -1007,6 +1009,7 @@ void submit(fpmgpu_context* ctx, HostSlot& sl, const fpmgpu_recon_request* req, 
             auto p = std::make_unique<fpmgpu_plan>();
             p->ctx = ctx;
             build_plan(*p, rb);
+            p->batch_tiles = req->num_tiles;  // the bands run concurrently: size kernels for the whole request
             sl.plans.push_back(p.release());
         }
         sl.band_t0 = t0;

@@ -713,7 +713,7 @@ static int loop_minb(int G, int T) {
 
 cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorMap* tmap, const LoopArgs& a, int T,
                           cudaStream_t s) {
-    const int minb = meas == kMeasTMA ? loop_minb(G, T) : 4;
+    const int minb = meas == kMeasTMA ? loop_minb(G, a.batch_T > 0 ? a.batch_T : T) : 4;
 #define FPM_LOOP_CASE(M, P, ME, GG, NN)                                                        \
     if (mode == M && prune == P && meas == ME && G == GG && a.N == NN) {                       \
         if (GG == 1 && ME == kMeasTMA && P && minb == 2)                                       \

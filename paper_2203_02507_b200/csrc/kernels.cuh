@@ -34,6 +34,7 @@ struct LoopArgs {
     int* work;                // nullptr: one CTA per tile, the whole slot range
     float* isum;              // [T][L] sum(I) of each LED's crop, formed by the pass-0 items
     int parts;                // work queue: items per pass (a pass's LED range cut into parts)
+    int batch_T;              // tiles sharing the GPU with this launch (concurrent bands); 0 = T
 };
 
 // Line FFTs for init_canvas / canvas_to_field (K2 / K3).

@@ -76,6 +76,9 @@ def test_online_wall_tracks_acquisition(eng):
     cfg = gpu_cfg(led_scan_rows=13, led_scan_cols=13)
     fs, _, seq, _ = dataset(cfg, seed=5)
     assert len(seq) == 169
+    # warm-up (context, lazily loaded kernels, plan buffers): the criterion is about
+    # keeping up with the stream, not about process start-up
+    fpm.run_online(fs, cfg, seq, fpm.RunOptions(iters=1), 0.0, engine=eng)
     t0 = time.perf_counter()
     res = fpm.run_online(fs, cfg, seq, fpm.RunOptions(iters=1), 0.05, engine=eng)
     wall = time.perf_counter() - t0
