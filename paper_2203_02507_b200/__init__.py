@@ -13,5 +13,8 @@ from .engine import (ConfigError, DataError, DomainError, Engine, FrameSet, Opti
                      spectrum_offset_px, stitch_mosaic, synthesized_na, tile_origins, update_step)
 
 from .forward import simulate_dataset  # noqa: F401,E402
+from .formats import (AppConfig, Dataset, IoError, NoiseSpec, RunConfig, config_from_json,  # noqa: F401,E402
+                      config_to_json, export_view, import_view, read_cfi, read_config, read_dataset, read_pgm16,
+                      write_cfi, write_config, write_dataset, write_pgm16)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -526,3 +526,32 @@ def test_seed_frame_missing_uses_brightest(orc, capsys):
     ref = orc.reconstruct_tile(ofs2, orc_cfg(cfg), 2, seq2)
     amp, ph = amp_phase_rel(got.hr, ref.hr)
     assert amp < PER_ITER_TOL and ph < PER_ITER_TOL, (amp, ph)
+
+
+def test_acceptance_criterion_7_format_hermeticity(tmp_path, eng):
+    """acceptance.cpp:311-359 through the formats module: a dataset directory
+    (frames/led_RR_CC.pgm + manifest.json) is read back and reconstructed twice;
+    the CFI outputs (4 tiles + the stitched mosaic) are bit-identical across the
+    runs, and CFI / PGM round trips are bit-exact."""
+    cfg = fpm.OpticalConfig(tile_size=64, tile_overlap=8, upsample=4, led_scan_rows=3, led_scan_cols=3)
+    fs, _, seq, obj = dataset(cfg, fov=120, seed=7)
+    fpm.write_dataset(tmp_path / "data", fs, cfg, object_truth=obj)
+    outs = {}
+    for run in ("run1", "run2"):
+        ds = fpm.read_dataset(tmp_path / "data")
+        res = fpm.run_offline(ds.frames, ds.cfg, fpm.led_sequence("spiral", ds.cfg), fpm.RunOptions(iters=2),
+                              engine=eng)
+        d = tmp_path / run
+        d.mkdir()
+        for i, t in enumerate(res.tiles):
+            fpm.write_cfi(d / f"tile_{i:03d}.cfi", t)
+        fpm.write_cfi(d / "stitched.cfi", res.stitched)
+        outs[run] = sorted(p.name for p in d.iterdir() if p.suffix == ".cfi")
+    assert outs["run1"] == outs["run2"] and len(outs["run1"]) >= 5
+    for name in outs["run1"]:
+        assert (tmp_path / "run1" / name).read_bytes() == (tmp_path / "run2" / name).read_bytes()
+    fpm.write_cfi(tmp_path / "rt.cfi", fpm.read_cfi(tmp_path / "run1" / "stitched.cfi"))
+    assert (tmp_path / "rt.cfi").read_bytes() == (tmp_path / "run1" / "stitched.cfi").read_bytes()
+    pgm = tmp_path / "data" / "frames" / "led_32_32.pgm"
+    fpm.write_pgm16(tmp_path / "rt.pgm", fpm.read_pgm16(pgm))
+    assert (tmp_path / "rt.pgm").read_bytes() == pgm.read_bytes()
