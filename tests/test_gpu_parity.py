@@ -555,3 +555,20 @@ def test_acceptance_criterion_7_format_hermeticity(tmp_path, eng):
     pgm = tmp_path / "data" / "frames" / "led_32_32.pgm"
     fpm.write_pgm16(tmp_path / "rt.pgm", fpm.read_pgm16(pgm))
     assert (tmp_path / "rt.pgm").read_bytes() == pgm.read_bytes()
+
+
+def test_acceptance_criterion_4_worker_and_batch_invariance(eng):
+    """acceptance.cpp:176-246 (a) on the device: the 16 tiles of a 232-px FOV are
+    identical for every worker count and for every batch size (max_tiles 4, 8,
+    12, 16 reconstruct the leading tiles of the same partition) — tiles share
+    nothing, and batch size only changes the kernel's schedule / build."""
+    cfg = gpu_cfg(led_scan_rows=5, led_scan_cols=5, tile_overlap=8)
+    fs, _, seq, _ = dataset(cfg, fov=232, seed=3)
+    ref = fpm.run_offline(fs, cfg, seq, fpm.RunOptions(iters=1, workers=1, max_tiles=16), engine=eng, stitch=False)
+    assert len(ref.tiles) == 16
+    for w in (2, 4, 8):
+        r = fpm.run_offline(fs, cfg, seq, fpm.RunOptions(iters=1, workers=w, max_tiles=16), engine=eng, stitch=False)
+        assert np.array_equal(r.tiles, ref.tiles)
+    for m in (4, 8, 12):
+        r = fpm.run_offline(fs, cfg, seq, fpm.RunOptions(iters=1, max_tiles=m), engine=eng, stitch=False)
+        assert np.array_equal(r.tiles, ref.tiles[:m])
