@@ -572,3 +572,25 @@ def test_acceptance_criterion_4_worker_and_batch_invariance(eng):
     for m in (4, 8, 12):
         r = fpm.run_offline(fs, cfg, seq, fpm.RunOptions(iters=1, max_tiles=m), engine=eng, stitch=False)
         assert np.array_equal(r.tiles, ref.tiles[:m])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strong_scaling_bands_bit_identical(eng, world):
+    """The strong-scaled data path (config 4/5) on one device: each rank's
+    tile-row band (distributed.shard_request: its tiles, y-shifted, over its
+    crop of the LR rows) reconstructs to the full FOV's tiles bit for bit."""
+    from paper_2203_02507_b200.distributed import shard_request
+    cfg = gpu_cfg(led_scan_rows=5, led_scan_cols=5, tile_overlap=8)
+    fs, _, seq, _ = dataset(cfg, fov=176, seed=39)
+    tiles = fpm.partition_tiles(fs.width(), fs.height(), cfg)
+    for t, d in zip(tiles, np.random.default_rng(9).uniform(-8, 8, len(tiles))):
+        t.defocus_um = float(d)
+    full = fpm.make_request(fs, cfg, seq, tiles, 2, mode="epry")
+    assert len(tiles) >= 3 * world
+    hr_full, res_full, _, _ = fpm.reconstruct_request(full, fs, engine=eng)
+    for r in range(world):
+        me = shard_request(full, r, world)
+        band = fpm.FrameSet(np.ascontiguousarray(fs.images[:, me.y_lo:me.y_hi, :]), fs.leds, fs.timestamps)
+        hr, res, _, _ = fpm.reconstruct_request(me.request, band, engine=eng)
+        assert np.array_equal(hr, hr_full[me.tiles])
+        assert np.array_equal(res, res_full[me.tiles])
