@@ -162,6 +162,17 @@ int fpmgpu_plan_execute(fpmgpu_plan* plan, const uint16_t* frames_dev, int64_t r
                         float* hr_dev, double* residuals_dev, float* pupils_out_dev, void* stream);
 int fpmgpu_plan_destroy(fpmgpu_plan* plan);
 
+/* run_offline's tiles + stitch_mosaic (parallel.cpp:170-183) in one pass when the
+ * plan's tiles abut without overlap on a full grid (stitch.cpp:38: zero overlap
+ * concatenates unscaled): canvas_to_field writes every HR field straight into
+ * the mosaic, tile t at row (y0 - y_min)*up, column (x0 - x_min)*up of mosaic_dev
+ * (mosaic_pitch elements per row). mosaic_dev may be a peer GPU's buffer
+ * (fpmgpu_ipc_open): each rank of a multi-GPU run then writes its band of the
+ * mosaic over NVLink. FPMGPU_ERR_UNSUPPORTED when the tiles overlap. */
+int fpmgpu_plan_execute_mosaic(fpmgpu_plan* plan, const uint16_t* frames_dev, int64_t row_pitch,
+                               float* mosaic_dev, int64_t mosaic_pitch, double* residuals_dev,
+                               float* pupils_out_dev, void* stream);
+
 typedef struct fpmgpu_plan_info {
     int tile_side, canvas_side, num_tiles, num_leds, iters, mode, lag, groups;
     int launches_per_execute;   /* kernels launched by one fpmgpu_plan_execute */
@@ -170,6 +181,7 @@ typedef struct fpmgpu_plan_info {
     double fft_flops_per_update;  /* 20 n^2 log2 n (nominal) */
     double hbm_bytes_per_update;  /* 2 n^2 + 16 |D| */
     int support_pixels;         /* |D| */
+    int tiles_abut;             /* 1: tiles on a full grid at stride n, no overlap (execute_mosaic) */
 } fpmgpu_plan_info;
 int fpmgpu_plan_get_info(const fpmgpu_plan* plan, fpmgpu_plan_info* info);
 
@@ -204,6 +216,54 @@ int fpmgpu_stitch_mosaic(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, 
 int fpmgpu_stitch_mosaic_device(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg,
                                 const float* tiles_dev, const int* xy, int num_tiles, float* out_dev,
                                 int* rows, int* cols, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU mosaic: stitch_mosaic (stitch.cpp:48-86) over tile-row bands, one
+ * band per rank. xy [T][2] lists the WHOLE FOV's tile origins (the same on every
+ * rank); a band is tiles [tile_lo, tile_hi) of that list and must be whole tile
+ * rows. Eq. (1)'s ratios form a chain across the FOV: each band computes its
+ * strips' row sums (sums), the ranks combine them (every rank needs every strip's
+ * sums: an all-reduce of zero-filled [strips][N] complex128 arrays is exact),
+ * and each band writes its own mosaic rows (assemble), straight into rank 0's
+ * mosaic over NVLink when mosaic_dev is a peer pointer. The single-GPU
+ * fpmgpu_stitch_mosaic is the one band of every tile: same arithmetic, same bits.
+ * ------------------------------------------------------------------------- */
+typedef struct fpmgpu_mosaic_band_info {
+    int rows, cols;              /* the whole mosaic */
+    int strips, strip_lo, strip_hi; /* tile rows; the band's [strip_lo, strip_hi) */
+    int row_lo, row_hi;          /* mosaic rows the band writes */
+    int canvas_side;             /* N */
+    int needs_exchange;          /* 0: every overlap is 0, ratios are 1, no sums needed */
+} fpmgpu_mosaic_band_info;
+/* host-only geometry query */
+int fpmgpu_mosaic_band_layout(const fpmgpu_optical_config* cfg, const int* xy, int num_tiles,
+                              int tile_lo, int tile_hi, fpmgpu_mosaic_band_info* info);
+/* tiles_dev: the band's HR tiles [tile_hi - tile_lo][N][N] complex64 (device).
+ * strip_sums [strips][N] complex128 (host): the band's strips are written, the
+ * others untouched; ratios [tile_hi - tile_lo] complex128 (host) out. Synchronous. */
+int fpmgpu_mosaic_band_sums(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const int* xy,
+                            int num_tiles, int tile_lo, int tile_hi, const float* tiles_dev,
+                            double* strip_sums, double* ratios, void* stream);
+/* strip_sums: every strip's sums (combined over the bands); ratios: this band's.
+ * mosaic_dev = row 0 of the whole mosaic (device, possibly a peer's), pitch in
+ * elements. Returns after the band's rows are written. */
+int fpmgpu_mosaic_band_assemble(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const int* xy,
+                                int num_tiles, int tile_lo, int tile_hi, const float* tiles_dev,
+                                const double* strip_sums, const double* ratios, float* mosaic_dev,
+                                int64_t mosaic_pitch, void* stream);
+
+/* CUDA IPC of a device buffer (rank 0's mosaic) to the other ranks' processes:
+ * handle = FPMGPU_IPC_HANDLE_BYTES opaque bytes naming dev_ptr's allocation,
+ * offset = dev_ptr's byte offset inside it (add it to the opened pointer). */
+#define FPMGPU_IPC_HANDLE_BYTES 64
+int fpmgpu_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset);
+int fpmgpu_ipc_open(fpmgpu_context* ctx, const void* handle, void** dev_ptr);
+int fpmgpu_ipc_close(fpmgpu_context* ctx, void* dev_ptr);
+
+/* Page-locked host buffers (outputs of the async host path must be page-locked
+ * for the copies to overlap; pageable outputs make the call synchronous). */
+int fpmgpu_host_alloc(int64_t bytes, void** ptr);
+int fpmgpu_host_free(void* ptr);
 
 #ifdef __cplusplus
 }

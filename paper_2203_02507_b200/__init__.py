@@ -12,6 +12,8 @@ from .engine import (ConfigError, DataError, DomainError, Engine, FrameSet, Opti
                      reconstruct_request, reconstruct_request_async, reconstruct_tile, run_offline, run_online, scan_leds, select_tiles, sequence_offsets,
                      spectrum_offset_px, stitch_mosaic, synthesized_na, tile_origins, update_step)
 
+from ._lib import CudaError, UnsupportedError  # noqa: F401,E402
+from .engine import pinned_empty  # noqa: F401,E402
 from .forward import simulate_dataset  # noqa: F401,E402
 from .formats import (AppConfig, Dataset, IoError, NoiseSpec, RunConfig, config_from_json,  # noqa: F401,E402
                       config_to_json, export_view, import_view, read_cfi, read_config, read_dataset, read_pgm16,

@@ -91,8 +91,18 @@ class PlanInfoC(C.Structure):
         ("iters", C.c_int), ("mode", C.c_int), ("lag", C.c_int), ("groups", C.c_int),
         ("launches_per_execute", C.c_int), ("loop_ctas", C.c_int), ("loop_threads", C.c_int),
         ("loop_smem_bytes", C.c_int), ("updates", C.c_double), ("fft_flops_per_update", C.c_double),
-        ("hbm_bytes_per_update", C.c_double), ("support_pixels", C.c_int),
+        ("hbm_bytes_per_update", C.c_double), ("support_pixels", C.c_int), ("tiles_abut", C.c_int),
     ]
+
+
+class MosaicBandInfoC(C.Structure):
+    _fields_ = [
+        ("rows", C.c_int), ("cols", C.c_int), ("strips", C.c_int), ("strip_lo", C.c_int), ("strip_hi", C.c_int),
+        ("row_lo", C.c_int), ("row_hi", C.c_int), ("canvas_side", C.c_int), ("needs_exchange", C.c_int),
+    ]
+
+
+IPC_HANDLE_BYTES = 64
 
 
 EXPORTS = [
@@ -104,7 +114,9 @@ EXPORTS = [
     "fpmgpu_plan_destroy", "fpmgpu_plan_get_info", "fpmgpu_plan_phase_times", "fpmgpu_update_step", "fpmgpu_init_canvas",
     "fpmgpu_canvas_to_field", "fpmgpu_stitch_mosaic", "fpmgpu_stitch_mosaic_device",
     "fpmgpu_online_begin", "fpmgpu_online_push", "fpmgpu_online_finish", "fpmgpu_online_destroy",
-    "fpmgpu_reconstruct_tiles_async", "fpmgpu_wait",
+    "fpmgpu_reconstruct_tiles_async", "fpmgpu_wait", "fpmgpu_plan_execute_mosaic", "fpmgpu_mosaic_band_layout",
+    "fpmgpu_mosaic_band_sums", "fpmgpu_mosaic_band_assemble", "fpmgpu_ipc_get_handle", "fpmgpu_ipc_open",
+    "fpmgpu_ipc_close", "fpmgpu_host_alloc", "fpmgpu_host_free",
 ]
 
 _lib: C.CDLL | None = None
@@ -146,6 +158,20 @@ def lib() -> C.CDLL:
         L.fpmgpu_stitch_mosaic_device.argtypes = [C.c_void_p, C.POINTER(OpticalConfigC), C.c_void_p, C.c_void_p,
                                                   C.c_int, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                                   C.c_void_p]
+        L.fpmgpu_plan_execute_mosaic.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                                 C.c_void_p, C.c_void_p, C.c_void_p]
+        L.fpmgpu_mosaic_band_layout.argtypes = [C.POINTER(OpticalConfigC), C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                                C.POINTER(MosaicBandInfoC)]
+        L.fpmgpu_mosaic_band_sums.argtypes = [C.c_void_p, C.POINTER(OpticalConfigC), C.c_void_p, C.c_int, C.c_int,
+                                              C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.fpmgpu_mosaic_band_assemble.argtypes = [C.c_void_p, C.POINTER(OpticalConfigC), C.c_void_p, C.c_int,
+                                                  C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                  C.c_int64, C.c_void_p]
+        L.fpmgpu_ipc_get_handle.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
+        L.fpmgpu_ipc_open.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.fpmgpu_ipc_close.argtypes = [C.c_void_p, C.c_void_p]
+        L.fpmgpu_host_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
+        L.fpmgpu_host_free.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 

@@ -264,6 +264,13 @@ struct fpmgpu_plan {
     DevBuf<int> work;     // LED-loop work queue: item counter + per-tile passes done
     DevBuf<float> isum;   // [T][L] sum(I) per crop (work-queue items of later passes)
     bool has_defocus = false, has_pupils = false;
+    // tiles abut without overlap on a full regular grid (stride n): the mosaic is a
+    // plain placement of the HR tiles, so canvas_to_field can write it directly
+    bool abut = false;
+    std::vector<int2> xy_host;
+    int x_min = 0, y_min = 0;
+    DevBuf<long long> out_off;
+    long long out_off_pitch = -1;
     // phase events of recent executes: [slot][4] = start, after init, after loop, after finalize
     static constexpr int kEventSlots = 256;
     std::vector<cudaEvent_t> events;
@@ -328,7 +335,7 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     p.bright.upload(bright.data(), bright.size(), p.ctx->stream);
     p.support_px = 0;
     for (auto s : sup) p.support_px += s;
-    p.cl = box_forced() ? 0 : cluster_choice(p.n, p.N, p.T);
+    p.cl = box_forced() ? 0 : cluster_choice(p.n, p.N, std::max(p.T, p.batch_tiles));
     if (p.cl) {
         box_of(sup, p.n, &p.b0, &p.box);
         std::vector<short2> runs(size_t(p.n), make_short2(0, 0));
@@ -401,6 +408,28 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     std::vector<int2> xy(static_cast<size_t>(p.T));
     for (int t = 0; t < p.T; ++t) xy[size_t(t)] = make_int2(r.tile_xy[2 * t], r.tile_xy[2 * t + 1]);
     p.tile_xy.upload(xy.data(), xy.size(), s);
+    {
+        std::vector<int> xs, ys;
+        for (auto& v : xy) {
+            xs.push_back(v.x);
+            ys.push_back(v.y);
+        }
+        std::sort(xs.begin(), xs.end());
+        xs.erase(std::unique(xs.begin(), xs.end()), xs.end());
+        std::sort(ys.begin(), ys.end());
+        ys.erase(std::unique(ys.begin(), ys.end()), ys.end());
+        bool ok = size_t(p.T) == xs.size() * ys.size();
+        for (size_t k = 1; k < xs.size(); ++k) ok &= xs[k] - xs[k - 1] == p.n;
+        for (size_t k = 1; k < ys.size(); ++k) ok &= ys[k] - ys[k - 1] == p.n;
+        std::vector<std::pair<int, int>> cells;
+        for (auto& v : xy) cells.emplace_back(v.y, v.x);
+        std::sort(cells.begin(), cells.end());
+        ok &= std::adjacent_find(cells.begin(), cells.end()) == cells.end();
+        p.abut = ok;
+        p.x_min = xs.front();
+        p.y_min = ys.front();
+        p.xy_host = xy;
+    }
     if (p.G > 1) p.slots.upload(slots.data(), slots.size(), s);
     p.has_defocus = r.tile_defocus_um != nullptr;
     if (p.has_defocus) p.defocus.upload(r.tile_defocus_um, size_t(p.T), s);
@@ -508,9 +537,30 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
 }
 
 // canvas_to_field: centered IFFT N x N * up^2 (the 1/N^2 of ifft2 folded in), recon.cpp:88-91
-void plan_epilogue(fpmgpu_plan& p, float* hr, float* pupils_out, cudaStream_t s) {
+// mosaic_pitch > 0: hr is a mosaic (row 0 = the plan's top tile row, column 0 =
+// its leftmost tile), tile t written at ((y0 - y_min) * up, (x0 - x_min) * up)
+void plan_epilogue(fpmgpu_plan& p, float* hr, float* pupils_out, cudaStream_t s, long long mosaic_pitch = 0) {
     const fpmgpu_recon_request& r = p.req;
     fpmk::LinesArgs la{};
+    if (mosaic_pitch > 0) {
+        if (!p.abut) throw Unsupported("the tiles overlap or leave gaps: stitch the HR tiles instead");
+        if (!hr) throw DataError("mosaic output missing");
+        if (mosaic_pitch < (long long)(p.N) * (long long)(p.xy_host.size())) {
+            long long w = 0;
+            for (auto& v : p.xy_host) w = std::max<long long>(w, (long long)(v.x - p.x_min) * r.cfg.upsample + p.N);
+            if (mosaic_pitch < w) throw DataError("mosaic pitch narrower than the band");
+        }
+        if (p.out_off_pitch != mosaic_pitch) {
+            std::vector<long long> off(p.xy_host.size());
+            for (size_t t = 0; t < off.size(); ++t)
+                off[t] = (long long)(p.xy_host[t].y - p.y_min) * r.cfg.upsample * mosaic_pitch +
+                         (long long)(p.xy_host[t].x - p.x_min) * r.cfg.upsample;
+            p.out_off.upload(off.data(), off.size(), s);
+            p.out_off_pitch = mosaic_pitch;
+        }
+        la.out_off = p.out_off.p;
+        la.out_pitch = mosaic_pitch;
+    }
     la.tw = p.ctx->twiddle_table(p.N);
     la.tile_xy = p.tile_xy.p;
     la.n = p.n;
@@ -518,7 +568,10 @@ void plan_epilogue(fpmgpu_plan& p, float* hr, float* pupils_out, cudaStream_t s)
     la.src = p.canvas.p;
     la.dst = p.canvas.p;
     la.scale = 1.0f;
+    const long long* off = la.out_off;
+    la.out_off = nullptr;
     ck(fpmk::launch_lines(2, p.N, la, p.T, s), "final rows");
+    la.out_off = off;
     la.dst = hr ? reinterpret_cast<float2*>(hr) : p.canvas.p;
     la.scale = float(double(r.cfg.upsample) * r.cfg.upsample / (double(p.N) * p.N));
     ck(fpmk::launch_lines(3, p.N, la, p.T, s), "final cols");
@@ -528,7 +581,7 @@ void plan_epilogue(fpmgpu_plan& p, float* hr, float* pupils_out, cudaStream_t s)
 }
 
 void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* hr, double* resid,
-                  float* pupils_out, cudaStream_t s) {
+                  float* pupils_out, cudaStream_t s, long long mosaic_pitch = 0) {
     cudaEvent_t* ev = p.slot_events();
     if (ev) ck(cudaEventRecord(ev[0], s), "event");
     plan_prologue(p, frames, pitch, s);
@@ -536,7 +589,7 @@ void execute_plan(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, float* 
     plan_loop(p, frames, pitch, resid, 0, p.num_slots, false, s);
     if (ev) ck(cudaEventRecord(ev[2], s), "event");
     // the pupil copy-out stays outside the finalize phase event
-    plan_epilogue(p, hr, nullptr, s);
+    plan_epilogue(p, hr, nullptr, s, mosaic_pitch);
     if (ev) ck(cudaEventRecord(ev[3], s), "event");
     if (pupils_out)
         ck(cudaMemcpyAsync(pupils_out, p.pupils.p, sizeof(float2) * size_t(p.T) * p.n * p.n,
@@ -661,76 +714,156 @@ StitchLayout stitch_layout(const Cfg& c, const int* xy, int T) {
 
 using C128 = std::complex<double>;
 
-// Ratios of the reference's mean_ratio chain from the per-tile sums, then the
-// assembly pass. colsum/rowsum come back to the host (2 x T x N complex128).
-void stitch_device(fpmgpu_context* ctx, StitchLayout lay, int N, const float2* tiles, float2* out, cudaStream_t s) {
-    const int T = int(lay.st.size());
+// A band of the mosaic: tiles [tile_lo, tile_hi) of the layout's tile list,
+// which must be whole strips (tile rows) [strip_lo, strip_hi). The band owns
+// mosaic rows [row_cut[strip_lo], row_cut[strip_hi]). The single-GPU stitch
+// is the band over every tile; a multi-GPU run gives each rank its band.
+struct MosaicBand {
+    StitchLayout lay;
+    int N = 0, tile_lo = 0, tile_hi = 0, strip_lo = 0, strip_hi = 0, row_lo = 0, row_hi = 0;
+    bool exchange = false;  // some overlap > 0: the ratios need the tiles' sums
+};
+
+MosaicBand mosaic_band(const Cfg& c, const int* xy, int T, int tile_lo, int tile_hi) {
+    MosaicBand b;
+    b.lay = stitch_layout(c, xy, T);
+    b.N = c.tile_size * c.upsample;
+    if (tile_lo < 0 || tile_hi > T || tile_lo >= tile_hi) throw DataError("mosaic band: empty or out-of-range tiles");
+    b.tile_lo = tile_lo;
+    b.tile_hi = tile_hi;
+    const StitchLayout& L = b.lay;
+    b.strip_lo = L.n_strips;
+    b.strip_hi = 0;
+    for (int s = 0; s < L.n_strips; ++s)
+        for (int k = 0; k < L.n_cols; ++k) {
+            const int t = L.grid[size_t(s) * L.n_cols + k];
+            if (t >= tile_lo && t < tile_hi) {
+                b.strip_lo = std::min(b.strip_lo, s);
+                b.strip_hi = std::max(b.strip_hi, s + 1);
+            }
+        }
+    int cnt = 0;
+    for (int s = b.strip_lo; s < b.strip_hi; ++s)
+        for (int k = 0; k < L.n_cols; ++k) {
+            const int t = L.grid[size_t(s) * L.n_cols + k];
+            if (t < tile_lo || t >= tile_hi) throw DataError("mosaic band: the tiles must be whole tile rows");
+            ++cnt;
+        }
+    if (cnt != tile_hi - tile_lo) throw DataError("mosaic band: the tiles must be whole tile rows");
+    b.row_lo = L.row_cut[size_t(b.strip_lo)];
+    b.row_hi = L.row_cut[size_t(b.strip_hi)];
+    for (int o : L.ovh) b.exchange |= o > 0;
+    for (int o : L.ovv) b.exchange |= o > 0;
+    return b;
+}
+
+// The band's tile table: the layout's entries of tiles [tile_lo, tile_hi), band-local.
+std::vector<fpmk::StitchTile> band_tiles(const MosaicBand& b) {
+    return std::vector<fpmk::StitchTile>(b.lay.st.begin() + b.tile_lo, b.lay.st.begin() + b.tile_hi);
+}
+
+// Phase 1 (per band): the horizontal mean_ratio chain of each of the band's strips
+// (stitch.cpp:60-70) -> ratio[t - tile_lo], and each strip's row sums
+// strip_sums[s][r] = sum_k ratio_k * rowsum_k[r] over its slots (the rows of the
+// assembled strip the vertical chain averages). Tiles' column / row sums come
+// from the device (complex128), the ratios are formed in double on the host.
+void band_sums(const MosaicBand& b, const float2* tiles, C128* strip_sums, C128* ratio, cudaStream_t s) {
+    const StitchLayout& lay = b.lay;
+    const int N = b.N, Tb = b.tile_hi - b.tile_lo;
+    for (int t = 0; t < Tb; ++t) ratio[t] = C128(1.0, 0.0);
+    if (!b.exchange) return;  // every overlap is 0: tiles concatenate unscaled (stitch.cpp:38)
+    const std::vector<fpmk::StitchTile> st = band_tiles(b);
     DevBuf<fpmk::StitchTile> st_d;
     DevBuf<double> colsum_d, rowsum_d;
-    st_d.upload(lay.st.data(), lay.st.size(), s);
-    colsum_d.ensure(size_t(T) * N * 2);
-    rowsum_d.ensure(size_t(T) * N * 2);
-    ck(fpmk::launch_stitch_sums(tiles, st_d.p, T, N, colsum_d.p, rowsum_d.p, s), "stitch sums");
-    std::vector<C128> colsum(size_t(T) * N), rowsum(size_t(T) * N);
+    st_d.upload(st.data(), st.size(), s);
+    colsum_d.ensure(size_t(Tb) * N * 2);
+    rowsum_d.ensure(size_t(Tb) * N * 2);
+    ck(fpmk::launch_stitch_sums(tiles, st_d.p, Tb, N, colsum_d.p, rowsum_d.p, s), "stitch sums");
+    std::vector<C128> colsum(size_t(Tb) * N), rowsum(size_t(Tb) * N);
     ck(cudaMemcpyAsync(colsum.data(), colsum_d.p, sizeof(C128) * colsum.size(), cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaMemcpyAsync(rowsum.data(), rowsum_d.p, sizeof(C128) * rowsum.size(), cudaMemcpyDeviceToHost, s), "D2H");
     ck(cudaStreamSynchronize(s), "stitch sums");
-    std::vector<C128> R(size_t(T), C128(1.0, 0.0)), S(size_t(lay.n_strips), C128(1.0, 0.0));
+    const int t0 = b.tile_lo;
     // horizontal: ratio of the strip's trailing overlap mean to the tile's leading mean
-    for (int sidx = 0; sidx < lay.n_strips; ++sidx)
+    for (int sidx = b.strip_lo; sidx < b.strip_hi; ++sidx)
         for (int k = 1; k < lay.n_cols; ++k) {
             const int o = lay.ovh[size_t(k)];
             if (o == 0) continue;  // zero overlap concatenates unscaled (stitch.cpp:38)
-            const int t = lay.grid[size_t(sidx) * lay.n_cols + k];
+            const int t = lay.grid[size_t(sidx) * lay.n_cols + k] - t0;
             C128 m1 = 0.0, m2 = 0.0;
             for (int C = lay.X[size_t(k)]; C < lay.X[size_t(k)] + o; ++C) {
                 // owner at the time tile k is joined: slot k-1 still reaches the strip's end
-                const int j = lay.grid[size_t(sidx) * lay.n_cols + std::min(lay.col_of[size_t(C)], k - 1)];
-                m1 += R[size_t(j)] * colsum[size_t(j) * N + (C - lay.st[size_t(j)].X)];
+                const int j = lay.grid[size_t(sidx) * lay.n_cols + std::min(lay.col_of[size_t(C)], k - 1)] - t0;
+                m1 += ratio[j] * colsum[size_t(j) * N + (C - st[size_t(j)].X)];
             }
             for (int q = 0; q < o; ++q) m2 += colsum[size_t(t) * N + q];
             const double cnt = double(N) * o;
             if (std::abs(m2 / cnt) < 1e-12) throw DataError("degenerate overlap: |mu2| vanishes");
-            R[size_t(t)] = m1 / m2;
+            ratio[t] = m1 / m2;
         }
-    // vertical: the same chain over strips (rows of the assembled strips)
-    auto strip_row = [&](int sidx, int r) {
-        C128 acc = 0.0;
-        for (int k = 0; k < lay.n_cols; ++k) {
-            const int j = lay.grid[size_t(sidx) * lay.n_cols + k];
-            acc += R[size_t(j)] * rowsum[size_t(j) * N + r];
+    for (int sidx = b.strip_lo; sidx < b.strip_hi; ++sidx)
+        for (int r = 0; r < N; ++r) {
+            C128 acc = 0.0;
+            for (int k = 0; k < lay.n_cols; ++k) {
+                const int j = lay.grid[size_t(sidx) * lay.n_cols + k] - t0;
+                acc += ratio[j] * rowsum[size_t(j) * N + r];
+            }
+            strip_sums[size_t(sidx) * N + r] = acc;
         }
-        return acc;
-    };
-    for (int k = 1; k < lay.n_strips; ++k) {
-        const int o = lay.ovv[size_t(k)];
-        if (o == 0) continue;
-        C128 m1 = 0.0, m2 = 0.0;
-        for (int Rr = lay.Y[size_t(k)]; Rr < lay.Y[size_t(k)] + o; ++Rr) {
-            const int so = std::min(lay.row_of[size_t(Rr)], k - 1);
-            m1 += S[size_t(so)] * strip_row(so, Rr - lay.Y[size_t(so)]);
+}
+
+// Phase 2 (per band, after every band's strip sums are in strip_sums): the
+// vertical mean_ratio chain over strips [0, strip_hi) (stitch.cpp:72-84), then
+// the band's mosaic rows written at out (row 0 of the whole mosaic, `pitch`
+// elements per row; a peer GPU's buffer for a multi-GPU mosaic).
+void band_assemble(const MosaicBand& b, const float2* tiles, const C128* strip_sums, const C128* ratio,
+                   float2* out, long long pitch, cudaStream_t s) {
+    const StitchLayout& lay = b.lay;
+    std::vector<C128> S(size_t(lay.n_strips), C128(1.0, 0.0));
+    if (b.exchange) {
+        const int N = b.N;
+        for (int k = 1; k < b.strip_hi; ++k) {
+            const int o = lay.ovv[size_t(k)];
+            if (o == 0) continue;
+            C128 m1 = 0.0, m2 = 0.0;
+            for (int Rr = lay.Y[size_t(k)]; Rr < lay.Y[size_t(k)] + o; ++Rr) {
+                const int so = std::min(lay.row_of[size_t(Rr)], k - 1);
+                m1 += S[size_t(so)] * strip_sums[size_t(so) * N + (Rr - lay.Y[size_t(so)])];
+            }
+            for (int r = 0; r < o; ++r) m2 += strip_sums[size_t(k) * N + r];
+            const double cnt = double(lay.cols) * o;
+            if (std::abs(m2 / cnt) < 1e-12) throw DataError("degenerate overlap: |mu2| vanishes");
+            S[size_t(k)] = m1 / m2;
         }
-        for (int r = 0; r < o; ++r) m2 += strip_row(k, r);
-        const double cnt = double(lay.cols) * o;
-        if (std::abs(m2 / cnt) < 1e-12) throw DataError("degenerate overlap: |mu2| vanishes");
-        S[size_t(k)] = m1 / m2;
     }
-    for (int sidx = 0; sidx < lay.n_strips; ++sidx)
+    std::vector<fpmk::StitchTile> st = band_tiles(b);
+    std::vector<int> grid;
+    for (int sidx = b.strip_lo; sidx < b.strip_hi; ++sidx)
         for (int k = 0; k < lay.n_cols; ++k) {
-            const int t = lay.grid[size_t(sidx) * lay.n_cols + k];
-            const C128 f = S[size_t(sidx)] * R[size_t(t)];
-            lay.st[size_t(t)].fre = float(f.real());
-            lay.st[size_t(t)].fim = float(f.imag());
+            const int t = lay.grid[size_t(sidx) * lay.n_cols + k] - b.tile_lo;
+            grid.push_back(t);
+            const C128 f = S[size_t(sidx)] * ratio[t];
+            st[size_t(t)].fre = float(f.real());
+            st[size_t(t)].fim = float(f.imag());
         }
+    DevBuf<fpmk::StitchTile> st_d;
     DevBuf<int> row_d, col_d, grid_d;
-    st_d.upload(lay.st.data(), lay.st.size(), s);
+    st_d.upload(st.data(), st.size(), s);
     row_d.upload(lay.row_of.data(), lay.row_of.size(), s);
     col_d.upload(lay.col_of.data(), lay.col_of.size(), s);
-    grid_d.upload(lay.grid.data(), lay.grid.size(), s);
-    ck(fpmk::launch_stitch_assemble(tiles, st_d.p, row_d.p, col_d.p, grid_d.p, lay.n_cols, N, lay.rows, lay.cols,
-                                    out, s), "stitch assemble");
+    grid_d.upload(grid.data(), grid.size(), s);
+    ck(fpmk::launch_stitch_assemble(tiles, st_d.p, row_d.p, col_d.p, grid_d.p, b.strip_lo, lay.n_cols, b.N, b.row_lo,
+                                    b.row_hi - b.row_lo, lay.cols, pitch, out, s), "stitch assemble");
     ck(cudaStreamSynchronize(s), "stitch assemble");  // the temporaries above are freed on return
-    (void)ctx;
+}
+
+// stitch_mosaic (stitch.cpp:48-86) on one GPU: the band of every tile.
+void stitch_device(const Cfg& c, const int* xy, int T, const float2* tiles, float2* out, cudaStream_t s) {
+    const MosaicBand b = mosaic_band(c, xy, T, 0, T);
+    std::vector<C128> sums(size_t(b.lay.n_strips) * b.N);
+    std::vector<C128> ratio(static_cast<size_t>(T));
+    band_sums(b, tiles, sums.data(), ratio.data(), s);
+    band_assemble(b, tiles, sums.data(), ratio.data(), out, b.lay.cols, s);
 }
 
 }  // namespace
@@ -902,6 +1035,16 @@ int fpmgpu_plan_execute(fpmgpu_plan* plan, const uint16_t* frames_dev, int64_t r
     });
 }
 
+int fpmgpu_plan_execute_mosaic(fpmgpu_plan* plan, const uint16_t* frames_dev, int64_t row_pitch, float* mosaic_dev,
+                               int64_t mosaic_pitch, double* residuals_dev, float* pupils_out_dev, void* stream) {
+    return guarded([&] {
+        if (mosaic_pitch < 1) throw DataError("mosaic pitch must be positive");
+        if (!plan->abut) throw Unsupported("the tiles overlap or leave gaps: stitch the HR tiles instead");
+        execute_plan(*plan, frames_dev, row_pitch, mosaic_dev, residuals_dev, pupils_out_dev,
+                     static_cast<cudaStream_t>(stream), mosaic_pitch);
+    });
+}
+
 int fpmgpu_plan_destroy(fpmgpu_plan* plan) {
     return guarded([&] { delete plan; });
 }
@@ -929,6 +1072,7 @@ int fpmgpu_plan_get_info(const fpmgpu_plan* p, fpmgpu_plan_info* info) {
         info->fft_flops_per_update = 20.0 * p->n * p->n * std::log2(double(p->n));
         info->hbm_bytes_per_update = 2.0 * p->n * p->n + 16.0 * p->support_px;
         info->support_pixels = p->support_px;
+        info->tiles_abut = p->abut ? 1 : 0;
     });
 }
 
@@ -1008,8 +1152,8 @@ void submit(fpmgpu_context* ctx, HostSlot& sl, const fpmgpu_recon_request* req, 
             if (req->pupils) rb.pupils = req->pupils + 2 * size_t(a) * req->cfg.tile_size * req->cfg.tile_size;
             auto p = std::make_unique<fpmgpu_plan>();
             p->ctx = ctx;
-            build_plan(*p, rb);
             p->batch_tiles = req->num_tiles;  // the bands run concurrently: size kernels for the whole request
+            build_plan(*p, rb);
             sl.plans.push_back(p.release());
         }
         sl.band_t0 = t0;
@@ -1070,9 +1214,17 @@ void submit(fpmgpu_context* ctx, HostSlot& sl, const fpmgpu_recon_request* req, 
         ck(cudaEventRecord(sl.arrived[b], s), "event");
         ck(cudaStreamWaitEvent(bs, sl.arrived[b], 0), "wait");
         fpmgpu_plan& pb = *sl.plans[b];
-        const size_t a = size_t(t0[b]), cnt = size_t(t0[b + 1] - t0[b]);
+        const size_t a = size_t(t0[b]);
         execute_plan(pb, fd, pitch, hr_d ? reinterpret_cast<float*>(hr_d + a * N * N) : nullptr, res_d + a * iters,
                      pup_d ? reinterpret_cast<float*>(pup_d + a * n * n) : nullptr, bs);
+    }
+    // Copies back only after every band's upload and kernels are enqueued: to
+    // pageable host memory a D2H cudaMemcpyAsync returns only when it is done,
+    // which would otherwise hold back the next band's upload until this band's
+    // reconstruction finished (pinned outputs overlap either way).
+    for (int b = 0; b < B; ++b) {
+        cudaStream_t bs = sl.streams[b];
+        const size_t a = size_t(t0[b]), cnt = size_t(t0[b + 1] - t0[b]);
         if (hr)
             ck(cudaMemcpyAsync(hr + 2 * a * N * N, hr_d + a * N * N, cnt * N * N * sizeof(float2),
                                cudaMemcpyDeviceToHost, bs), "hr D2H");
@@ -1402,7 +1554,7 @@ int fpmgpu_stitch_mosaic(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, 
         DevBuf<float2> t_d, o_d;
         t_d.upload(reinterpret_cast<const float2*>(tiles), size_t(num_tiles) * N * N, ctx->stream);
         o_d.ensure(size_t(lay.rows) * lay.cols);
-        stitch_device(ctx, lay, N, t_d.p, o_d.p, ctx->stream);
+        stitch_device(*cfg, xy, num_tiles, t_d.p, o_d.p, ctx->stream);
         ck(cudaMemcpyAsync(out, o_d.p, sizeof(float2) * size_t(lay.rows) * lay.cols, cudaMemcpyDeviceToHost,
                            ctx->stream), "mosaic D2H");
         ck(cudaStreamSynchronize(ctx->stream), "stitch_mosaic");
@@ -1417,9 +1569,97 @@ int fpmgpu_stitch_mosaic_device(fpmgpu_context* ctx, const fpmgpu_optical_config
         *cols = lay.cols;
         if (!out_dev) return;
         ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-        stitch_device(ctx, lay, cfg->tile_size * cfg->upsample, reinterpret_cast<const float2*>(tiles_dev),
+        stitch_device(*cfg, xy, num_tiles, reinterpret_cast<const float2*>(tiles_dev),
                       reinterpret_cast<float2*>(out_dev), static_cast<cudaStream_t>(stream));
     });
+}
+
+int fpmgpu_mosaic_band_layout(const fpmgpu_optical_config* cfg, const int* xy, int num_tiles, int tile_lo,
+                              int tile_hi, fpmgpu_mosaic_band_info* info) {
+    return guarded([&] {
+        const MosaicBand b = mosaic_band(*cfg, xy, num_tiles, tile_lo, tile_hi);
+        info->rows = b.lay.rows;
+        info->cols = b.lay.cols;
+        info->strips = b.lay.n_strips;
+        info->strip_lo = b.strip_lo;
+        info->strip_hi = b.strip_hi;
+        info->row_lo = b.row_lo;
+        info->row_hi = b.row_hi;
+        info->canvas_side = b.N;
+        info->needs_exchange = b.exchange ? 1 : 0;
+    });
+}
+
+int fpmgpu_mosaic_band_sums(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const int* xy, int num_tiles,
+                            int tile_lo, int tile_hi, const float* tiles_dev, double* strip_sums, double* ratios,
+                            void* stream) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const MosaicBand b = mosaic_band(*cfg, xy, num_tiles, tile_lo, tile_hi);
+        band_sums(b, reinterpret_cast<const float2*>(tiles_dev), reinterpret_cast<C128*>(strip_sums),
+                  reinterpret_cast<C128*>(ratios), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fpmgpu_mosaic_band_assemble(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, const int* xy, int num_tiles,
+                                int tile_lo, int tile_hi, const float* tiles_dev, const double* strip_sums,
+                                const double* ratios, float* mosaic_dev, int64_t mosaic_pitch, void* stream) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const MosaicBand b = mosaic_band(*cfg, xy, num_tiles, tile_lo, tile_hi);
+        if (mosaic_pitch < b.lay.cols) throw DataError("mosaic pitch narrower than the mosaic");
+        band_assemble(b, reinterpret_cast<const float2*>(tiles_dev), reinterpret_cast<const C128*>(strip_sums),
+                      reinterpret_cast<const C128*>(ratios), reinterpret_cast<float2*>(mosaic_dev), mosaic_pitch,
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fpmgpu_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset) {
+    return guarded([&] {
+        static_assert(sizeof(cudaIpcMemHandle_t) == FPMGPU_IPC_HANDLE_BYTES, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)), "cudaIpcGetMemHandle");
+        std::memcpy(handle, &h, sizeof(h));
+        // the handle names the whole allocation: report where dev_ptr sits in it
+        static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+        static std::once_flag once;
+        std::call_once(once, [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+        });
+        if (!range) throw CudaError("cuMemGetAddressRange unavailable");
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (range(&base, &size, CUdeviceptr(dev_ptr)) != CUDA_SUCCESS) throw CudaError("cuMemGetAddressRange failed");
+        *offset = int64_t(CUdeviceptr(dev_ptr) - base);
+    });
+}
+
+int fpmgpu_ipc_open(fpmgpu_context* ctx, const void* handle, void** dev_ptr) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        ck(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+int fpmgpu_ipc_close(fpmgpu_context* ctx, void* dev_ptr) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        ck(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+    });
+}
+
+int fpmgpu_host_alloc(int64_t bytes, void** ptr) {
+    return guarded([&] { ck(cudaHostAlloc(ptr, size_t(std::max<int64_t>(bytes, 1)), cudaHostAllocPortable), "cudaHostAlloc"); });
+}
+
+int fpmgpu_host_free(void* ptr) {
+    return guarded([&] { ck(cudaFreeHost(ptr), "cudaFreeHost"); });
 }
 
 }  // extern "C"

@@ -47,6 +47,11 @@ struct LinesArgs {
     const int2* tile_xy;      // [T]
     int n, up;
     float scale;
+    // finalize cols only: tile t's HR field written at dst + out_off[t] with row
+    // pitch out_pitch (elements) — straight into a mosaic (or a peer GPU's
+    // mosaic) when the tiles abut without overlap; nullptr = dst[t][N][N]
+    const long long* out_off;
+    long long out_pitch;
 };
 
 // General tile sides (n = 64, 128, 256): warp-FFT row/column passes over the

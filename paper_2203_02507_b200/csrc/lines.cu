@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(256) lines_fft(const LinesArgs a) {
             const int i = e, j = l0 + line;
             float2 x = res[line * NL + e];
             const float sc = ((i + j) & 1) ? -a.scale : a.scale;
-            a.dst[base + size_t(i) * NL + j] = cscale(x, sc);
+            const size_t o = (WHICH == 3 && a.out_off) ? size_t(a.out_off[tile]) + size_t(i) * a.out_pitch + j
+                                                       : base + size_t(i) * NL + j;
+            a.dst[o] = cscale(x, sc);
         } else {
             const int line = idx / NL, e = idx - line * NL;
             a.dst[base + size_t(l0 + line) * NL + e] = res[line * NL + e];
@@ -234,7 +236,9 @@ __global__ void __launch_bounds__(512) lines_fft_w256(const LinesArgs a) {
             float2 x = s[line * LS + pad(e)];
             if (INV) x.y = -x.y;
             const float sc = ((i + j) & 1) ? -a.scale : a.scale;
-            a.dst[base + size_t(i) * NL + j] = cscale(x, sc);
+            const size_t o = (WHICH == 3 && a.out_off) ? size_t(a.out_off[tile]) + size_t(i) * a.out_pitch + j
+                                                       : base + size_t(i) * NL + j;
+            a.dst[o] = cscale(x, sc);
         } else {
             const int line = idx / NL, e = idx - line * NL;
             float2 x = s[line * LS + pad(e)];

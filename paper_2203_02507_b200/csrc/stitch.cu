@@ -60,19 +60,22 @@ __global__ void stitch_rowsum_kernel(const float2* __restrict__ tiles, const Sti
     }
 }
 
-// Mosaic pixel (R, C): owner tile via the strip/slot interval tables.
+// Mosaic pixel (R, C), R in [row0, row0 + nrows): owner tile via the strip/slot
+// interval tables; grid holds the band's strips [strip0, ...) with band-local
+// tile indices. out is the mosaic's row 0 (pitch in elements; a peer GPU's
+// mosaic when the band is written over NVLink).
 __global__ void stitch_assemble_kernel(const float2* __restrict__ tiles, const StitchTile* __restrict__ st,
                                        const int* __restrict__ row_of, const int* __restrict__ col_of,
-                                       const int* __restrict__ grid, int n_cols, int N, int rows, int cols,
-                                       float2* __restrict__ out) {
-    const size_t total = size_t(rows) * cols;
+                                       const int* __restrict__ grid, int strip0, int n_cols, int N, int row0,
+                                       int nrows, int cols, long long pitch, float2* __restrict__ out) {
+    const size_t total = size_t(nrows) * cols;
     for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
          idx += size_t(gridDim.x) * blockDim.x) {
-        const int R = int(idx / cols), Cc = int(idx % cols);
-        const int t = grid[row_of[R] * n_cols + col_of[Cc]];
+        const int R = row0 + int(idx / cols), Cc = int(idx % cols);
+        const int t = grid[(row_of[R] - strip0) * n_cols + col_of[Cc]];
         const StitchTile s = st[t];
         const float2 v = tiles[size_t(t) * N * N + size_t(R - s.Y) * N + (Cc - s.X)];
-        out[idx] = cmul(v, make_float2(s.fre, s.fim));
+        out[size_t(R) * pitch + Cc] = cmul(v, make_float2(s.fre, s.fim));
     }
 }
 
@@ -90,11 +93,13 @@ cudaError_t launch_stitch_sums(const float2* tiles, const StitchTile* st, int T,
 }
 
 cudaError_t launch_stitch_assemble(const float2* tiles, const StitchTile* st, const int* row_of, const int* col_of,
-                                   const int* grid, int n_cols, int N, int rows, int cols, float2* out,
-                                   cudaStream_t s) {
-    const size_t total = size_t(rows) * cols;
+                                   const int* grid, int strip0, int n_cols, int N, int row0, int nrows, int cols,
+                                   long long pitch, float2* out, cudaStream_t s) {
+    const size_t total = size_t(nrows) * cols;
+    if (total == 0) return cudaSuccess;
     const int blocks = int(std::min<size_t>((total + 255) / 256, size_t(148) * 32));
-    stitch_assemble_kernel<<<blocks, 256, 0, s>>>(tiles, st, row_of, col_of, grid, n_cols, N, rows, cols, out);
+    stitch_assemble_kernel<<<blocks, 256, 0, s>>>(tiles, st, row_of, col_of, grid, strip0, n_cols, N, row0, nrows,
+                                                  cols, pitch, out);
     return cudaGetLastError();
 }
 

@@ -441,16 +441,29 @@ class PendingReconstruction:
         return hr, res, pup, lag.value
 
 
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A numpy array in page-locked host memory (fpmgpu_host_alloc), freed with the array."""
+    import weakref
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    ptr = C.c_void_p()
+    check(lib().fpmgpu_host_alloc(max(nbytes, 1), C.byref(ptr)))
+    buf = (C.c_char * max(nbytes, 1)).from_address(ptr.value)
+    weakref.finalize(buf, lib().fpmgpu_host_free, C.c_void_p(ptr.value))
+    return np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+
 def reconstruct_request_async(req: Request, frames: FrameSet, engine: Engine | None = None) -> PendingReconstruction:
     """fpmgpu_reconstruct_tiles_async: the request's LR upload may overlap the
-    previous request's reconstruction (two in flight per engine)."""
+    previous request's reconstruction (two in flight per engine). The outputs
+    live in page-locked memory, so their copies back are asynchronous too."""
     eng = engine or default_engine()
     r, keep = req.c()
     T, n, N = r.num_tiles, req.cfg.tile_size, req.cfg.hr_size()
     imgs = np.ascontiguousarray(frames.images, np.uint16)
-    hr = np.zeros((T, N, N), np.complex64)
-    res = np.zeros((T, req.iters), np.float64)
-    pup = np.zeros((T, n, n), np.complex64)
+    hr = pinned_empty((T, N, N), np.complex64)
+    res = pinned_empty((T, req.iters), np.float64)
+    pup = pinned_empty((T, n, n), np.complex64)
     t = C.c_longlong()
     check(lib().fpmgpu_reconstruct_tiles_async(eng.handle, C.byref(r), imgs.ctypes.data, imgs.shape[2],
                                                hr.ctypes.data, res.ctypes.data, pup.ctypes.data, C.byref(t)))
@@ -680,6 +693,14 @@ class Plan:
                 pupils_ptr: int | None = None, stream: int | None = None) -> None:
         check(lib().fpmgpu_plan_execute(self._h, frames_ptr, int(row_pitch), hr_ptr, residuals_ptr, pupils_ptr,
                                         stream))
+
+    def execute_mosaic(self, frames_ptr: int, row_pitch: int, mosaic_ptr: int, mosaic_pitch: int,
+                       residuals_ptr: int | None, pupils_ptr: int | None = None, stream: int | None = None) -> None:
+        """execute() with the HR fields written straight into a mosaic (tiles that
+        abut without overlap: stitch_mosaic is a plain placement, stitch.cpp:38).
+        mosaic_ptr is the plan's top-left tile position, pitch in complex64 elements."""
+        check(lib().fpmgpu_plan_execute_mosaic(self._h, frames_ptr, int(row_pitch), mosaic_ptr, int(mosaic_pitch),
+                                               residuals_ptr, pupils_ptr, stream))
 
     def phase_times(self, reset: bool = True):
         """(ms_init, ms_loop, ms_final) summed over executes since the last reset, and the execute count."""

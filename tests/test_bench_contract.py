@@ -24,3 +24,20 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and "sample" in cb
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # the reference arm runs the oracle restatement only: the product library is never mapped
+    assert d["repo_native_libs_loaded"] == ["oracle/lib/libfpm_oracle.so"], d["repo_native_libs_loaded"]
+    assert d["scaling"] == "strong" and d["config"]["updates_per_step_all_ranks"] == 2304000
+
+
+def test_config_blocks_identical_across_arms():
+    """Both arms print the same config block for the same (N, scaling): the
+    driver's ratio needs same_config."""
+    sys.path.insert(0, ROOT)
+    import bench
+    W = bench.WORKLOADS[3]
+    for world in (1, 2, 8):
+        for scaling in ("strong", "weak"):
+            a = bench.config_block(W, world, scaling)
+            assert a == bench.config_block(W, world, scaling)
+            assert a["updates_per_step_all_ranks"] == W.updates * (world if scaling == "weak" else 1)
+    assert bench.config_block(W, 8, "strong")["baseline_config"] == 4
