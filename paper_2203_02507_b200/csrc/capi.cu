@@ -183,12 +183,18 @@ int cluster_choice(int n, int N, int T) {
     return 0;
 }
 
-// FPM_B200_W64=1 runs n = 64 one warp per tile (kernels_w64.cu). Opt-in: at 8
-// warps per SM it is latency- and instruction-cache-bound (config 3 loop 148 ms
-// vs 32 ms for the 128-thread lattice kernel).
-bool w64_choice(int /*T*/) {
-    const char* e = std::getenv("FPM_B200_W64");
-    return e && e[0] == '1';
+// n = 64 on 256 threads per tile (kernels_quad.cu) for strong-scaled batches of at
+// most one tile per SM: a lone tile's update is latency-bound and twice the warps
+// shorten it (config 3 over 8 GPUs, 128 tiles per rank: 9.00 -> 7.93 ms); with more
+// tiles per SM the 128-thread pair lattice wins (fewer shuffles: 1,024 tiles 33.2 vs
+// 44.2 ms, tools/quad_probe.sh). Batches below 64 tiles (single tiles, small FOVs) stay
+// on the pair lattice, whose sequential runs are bit-identical to the pipelined
+// schedule (test_parallel.cpp:97-108). FPM_B200_QUAD=1|0 forces.
+bool quad_choice(int T) {
+    if (const char* e = std::getenv("FPM_B200_QUAD"); e && e[0]) return e[0] == '1';
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return T >= 64 && T <= sms;
 }
 
 std::vector<float2> twiddles(int N) {
@@ -247,7 +253,7 @@ struct fpmgpu_plan {
     int n = 0, N = 0, T = 0, L = 0, F = 0, G = 1, lag = 0, nslots = 1, num_slots = 0;
     bool prune = false;
     bool use_box = false;  // n != 64: warp-FFT box kernel (kernels_box.cu)
-    bool w64 = false;      // n = 64, sequential, disk inside [16, 48): one warp per tile (kernels_w64.cu)
+    bool quad = false;     // n = 64, sequential, disk inside [16, 48): 256 threads per tile (kernels_quad.cu)
     int cl = 0;            // > 0: each tile split over a cluster of cl CTAs (kernels_cluster.cu)
     int box = 0, b0 = 0;
     int support_px = 0;
@@ -398,8 +404,8 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
         }
     }
     p.num_slots = p.G == 1 ? r.iters * p.L : int(slots.size() / 2);
-    p.w64 = !p.use_box && !p.cl && p.prune && p.G == 1 && w64_choice(p.T) &&
-            fpmk::loop_w64_smem_bytes(p.L, r.iters) <= 227 * 1024;
+    p.quad = !p.use_box && !p.cl && p.prune && p.G == 1 &&
+             quad_choice(std::max(p.T, p.batch_tiles)) && fpmk::loop64q_smem_bytes(p.L, r.iters, true) <= 227 * 1024;
 
     cudaStream_t s = p.ctx->stream;
     p.support.upload(sup.data(), sup.size(), s);
@@ -501,6 +507,11 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
     a.alpha = float(r.alpha);
     a.beta = float(r.beta);
     a.batch_T = p.batch_tiles > 0 ? p.batch_tiles : p.T;
+    if (const char* j = std::getenv("FPM_B200_JITTER"); j && j[0]) {  // race hunting (kernels.cuh)
+        a.jitter = std::max(0, std::atoi(j));
+        const char* c = std::strchr(j, ':');
+        a.jitter_seed = c ? unsigned(std::strtoul(c + 1, nullptr, 10)) : 1u;
+    }
     if (p.use_box || p.cl) {
         fpmk::BoxArgs bx{};
         bx.scratch = p.scratch.p;
@@ -516,23 +527,16 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
             ck(fpmk::launch_loop_cluster(p.n, r.mode, p.cl, a, bx, p.T, s), "LED loop (cluster)");
         else
             ck(fpmk::launch_loop_box(p.n, r.mode, a, bx, p.T, s), "LED loop (box)");
-    } else if (p.w64) {
-        fpmk::BoxArgs bx{};
-        bx.frames = frames;
-        bx.pitch = pitch;
-        bx.frame_stride = pitch * r.height;
-        if (s0 == 0 && s1 == p.num_slots && !acc) {  // whole run: the work queue may serve it
-            a.work = p.work.ensure(size_t(p.T) + 1);
-            a.isum = p.isum.ensure(size_t(p.T) * p.L);
-        }
-        ck(fpmk::launch_loop_w64(r.mode, a, bx, p.T, s), "LED loop (warp per tile)");
     } else {
         const CUtensorMap map = encode_frames_map(frames, p.F, r.height, r.width, pitch);
         if (p.G == 1 && s0 == 0 && s1 == p.num_slots && !acc) {  // whole run: the work queue may serve it
             a.work = p.work.ensure(size_t(p.T) + 1);
             a.isum = p.isum.ensure(size_t(p.T) * p.L);
         }
-        ck(fpmk::launch_loop64(r.mode, p.prune, fpmk::kMeasTMA, p.G, &map, a, p.T, s), "LED loop");
+        if (p.quad)
+            ck(fpmk::launch_loop64q(r.mode, &map, a, p.T, s), "LED loop (quad)");
+        else
+            ck(fpmk::launch_loop64(r.mode, p.prune, fpmk::kMeasTMA, p.G, &map, a, p.T, s), "LED loop");
     }
 }
 
@@ -610,8 +614,8 @@ bool same_request(const HostSlot& c, const fpmgpu_recon_request& r, std::vector<
     ki.insert(ki.end(), r.seq_frame, r.seq_frame + r.num_leds);
     // kernel-selection overrides change the plans too
     const char* cl_env = std::getenv("FPM_B200_CLUSTER");
-    const char* w_env = std::getenv("FPM_B200_W64");
-    ki.insert(ki.end(), {box_forced() ? 1 : 0, cl_env ? std::atoi(cl_env) : -1, w_env && w_env[0] ? w_env[0] : -1});
+    const char* q_env = std::getenv("FPM_B200_QUAD");
+    ki.insert(ki.end(), {box_forced() ? 1 : 0, cl_env ? std::atoi(cl_env) : -1, q_env && q_env[0] ? q_env[0] : -1});
     kd.push_back(r.alpha);
     kd.push_back(r.beta);
     if (r.tile_defocus_um) kd.insert(kd.end(), r.tile_defocus_um, r.tile_defocus_um + r.num_tiles);
@@ -1062,11 +1066,12 @@ int fpmgpu_plan_get_info(const fpmgpu_plan* p, fpmgpu_plan_info* info) {
         info->groups = p->G;
         info->launches_per_execute = (p->has_pupils ? 0 : 1) + 2 + 1 + 2;
         info->loop_ctas = p->T * (p->cl ? p->cl : 1);
-        info->loop_threads = p->cl ? 32 * fpmk::cluster_warps(p->n, p->cl) : p->use_box ? 512 : 128 * p->G;
+        info->loop_threads = p->cl ? 32 * fpmk::cluster_warps(p->n, p->cl) : p->use_box ? 512 : p->quad ? 256 : 128 * p->G;
         info->loop_smem_bytes =
             int(p->cl ? fpmk::cluster_smem_bytes(p->n, p->box, p->cl, fpmk::cluster_warps(p->n, p->cl), p->L,
                                                  p->req.iters)
                 : p->use_box ? fpmk::box_smem_bytes(p->n, p->box, p->L, p->req.iters, p->n != 256)
+                : p->quad    ? fpmk::loop64q_smem_bytes(p->L, p->req.iters, true)
                              : fpmk::loop_smem_bytes(p->G, p->nslots, p->L, p->req.iters));
         info->updates = double(p->T) * p->L * p->req.iters;
         info->fft_flops_per_update = 20.0 * p->n * p->n * std::log2(double(p->n));

@@ -31,6 +31,7 @@
 
 #include "fft_device.cuh"
 #include "kernels.cuh"
+#include "ptx_util.cuh"
 
 namespace fpmk {
 
@@ -56,51 +57,6 @@ constexpr int kGroupThreads = 128;
 #ifndef FPM_LOOP_MINB
 #define FPM_LOOP_MINB 4  // resident tiles per SM the register budget is sized for
 #endif
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@P1 bra DONE;\n"
-        "bra WAIT;\n"
-        "DONE:\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-// 3-D tiled TMA load of one 64x64 u16 LR crop: coordinates (x, y, frame).
-__device__ __forceinline__ void tma_load_crop(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int f) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(f)
-        : "memory");
-}
-
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // Barrier over one 128-thread group (named barrier 1 + g).
 __device__ __forceinline__ void group_sync(int g) {
@@ -369,6 +325,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                 __threadfence();
                 st_release_gpu(args.work + 1 + jp % args.T, jp / args.T + 1);
             }
+            jitter_sleep(args, -1 - round);
             const int j = atomicAdd(args.work, 1);
             *item_s = j;
             if (j < n_items && j >= args.T) {  // acquire: the tile's previous pass is complete
@@ -429,6 +386,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     // sequential slots (G == 1): (iteration, position) by counters, not a division per slot
     int c_it = G == 1 ? s_begin / L : 0, c_pos = G == 1 ? s_begin - c_it * L : 0;
     for (int s = s_begin; s < s_end; ++s) {
+        jitter_sleep(args, s);
         const int2 e = G == 1 ? make_int2(c_it, c_pos) : slot_entry<G>(args, s, g);
         if (e.x >= 0) {
             if (!issued) issue(e);

@@ -35,6 +35,8 @@ struct LoopArgs {
     float* isum;              // [T][L] sum(I) of each LED's crop, formed by the pass-0 items
     int parts;                // work queue: items per pass (a pass's LED range cut into parts)
     int batch_T;              // tiles sharing the GPU with this launch (concurrent bands); 0 = T
+    int jitter;               // > 0: race hunting, every warp sleeps 0..jitter ns per update / item
+    unsigned jitter_seed;
 };
 
 // Line FFTs for init_canvas / canvas_to_field (K2 / K3).
@@ -76,12 +78,28 @@ cudaError_t launch_loop_cluster(int n, int mode, int cl, const LoopArgs& a, cons
 
 size_t loop_smem_bytes(int G, int nslots, int L, int iters);
 
-// n = 64, one warp per tile (kernels_w64.cu): sequential schedules whose pupil
-// disk lies in rows/cols [16, 48) of the block.
-size_t loop_w64_smem_bytes(int L, int iters);
-cudaError_t launch_loop_w64(int mode, const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s);
+// n = 64 with 256 threads per tile (kernels_quad.cu): sequential schedules whose
+// pupil disk lies in rows/cols [16, 48) of the block, TMA-staged measurements.
+size_t loop64q_smem_bytes(int L, int iters, bool osep);
+cudaError_t launch_loop64q(int mode, const CUtensorMap* tmap, const LoopArgs& a, int T, cudaStream_t s);
+
 
 #ifdef __CUDACC__
+// Schedule perturbation for race hunting (FPM_B200_JITTER=<ns>[:<seed>]): each warp
+// sleeps a pseudo-random 0..jitter ns before every update and work-queue claim, so a
+// missing barrier, fence or dependency wait shows up as run-to-run bit differences
+// (tests/test_race_jitter.py; compute-sanitizer is closed on the GPU pool).
+__device__ __forceinline__ void jitter_sleep(const LoopArgs& a, int step) {
+    if (a.jitter > 0) {
+        unsigned h = a.jitter_seed ^ (blockIdx.x * 0x9E3779B1u) ^ (unsigned(step) * 0x85EBCA77u) ^
+                     ((threadIdx.x >> 5) * 0xC2B2AE3Du);
+        h ^= h >> 15;
+        h *= 0x2C1B3C6Du;
+        h ^= h >> 12;
+        __nanosleep(h % unsigned(a.jitter));
+    }
+}
+
 // Per-pass mean residuals of the stages a launch touched (all of them for a
 // whole run; a stage range for the online passes, accumulated).
 __device__ __forceinline__ void store_residuals(const LoopArgs& a, int tile, const double* stage_sum, bool ranged) {

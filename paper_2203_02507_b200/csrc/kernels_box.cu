@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
     // the whole CTA — they touch disjoint disks, so any order equals the concurrent one
     const int G = args.slots ? 2 : 1;
     for (int e = args.slot_begin * G; e < args.num_slots * G; ++e) {
+        jitter_sleep(args, e);
         int it, pos;
         if (G == 1) {
             it = e / L;

@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(args.work + 1 + jp % args.T), "r"(jp / args.T + 1)
                              : "memory");
             }
+            jitter_sleep(args, -1 - round);
             const int j = atomicAdd(args.work, 1);
             if (j < n_items && j >= args.T) {  // acquire: the tile's previous pass is complete
                 const int* flag = args.work + 1 + (j % args.T);
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         stage(pos0);
     }
     for (; e >= 0;) {
+        jitter_sleep(args, e);
         int it, pos;
         entry_at(e, it, pos);
         float2* const S = par ? S1 : S0;

@@ -175,15 +175,17 @@ def test_multi_tile_batch_matches_oracle(orc, eng):
         assert amp < FINAL_TOL and ph < FINAL_TOL, (i, amp, ph)
 
 
-W64_DATA = {"gs": dict(rows=15, seed=1, defocus=0.0), "epry": dict(rows=9, seed=5, defocus=25.0)}
+QUAD_DATA = {"gs": dict(rows=15, seed=1, defocus=0.0), "epry": dict(rows=9, seed=5, defocus=25.0)}
 
 
 @pytest.mark.parametrize("mode,iters", [("gs", 1), ("gs", 2), ("gs", 10), ("epry", 1), ("epry", 3)])
-def test_warp_kernel_matches_oracle(orc, eng, monkeypatch, mode, iters):
-    """n = 64 on the one-warp-per-tile kernel (kernels_w64.cu, forced for one tile)
-    against the oracle: 1e-4 per iteration, 1e-3 after the full count (config 1)."""
-    monkeypatch.setenv("FPM_B200_W64", "1")
-    d = W64_DATA[mode]
+@pytest.mark.parametrize("quad", ["0", "1"])
+def test_n64_kernels_match_oracle(orc, eng, monkeypatch, mode, iters, quad):
+    """n = 64 on the 128-thread pair lattice (kernels.cu) and on the 256-thread quad
+    lattice (kernels_quad.cu), each forced, against the oracle: 1e-4 per iteration,
+    1e-3 after the full count (config 1)."""
+    monkeypatch.setenv("FPM_B200_QUAD", quad)
+    d = QUAD_DATA[mode]
     cfg = gpu_cfg(led_scan_rows=d["rows"], led_scan_cols=d["rows"], tile_overlap=0)
     fs, ofs, seq, _ = dataset(cfg, seed=d["seed"], defocus_um=d["defocus"])
     t = fpm.partition_tiles(64, 64, cfg)[0]
@@ -198,10 +200,11 @@ def test_warp_kernel_matches_oracle(orc, eng, monkeypatch, mode, iters):
 
 
 @pytest.mark.parametrize("queue", ["0", "1"])
-def test_warp_kernel_multi_tile_batch(orc, eng, monkeypatch, queue):
-    """Per-tile k-vectors and defocus pupils on the warp kernel, one CTA per tile
-    and as the work queue, against the oracle; the two schedules agree bit for bit."""
-    monkeypatch.setenv("FPM_B200_W64", "1")
+def test_quad_kernel_multi_tile_batch(orc, eng, monkeypatch, queue):
+    """Per-tile k-vectors and defocus pupils on the quad-lattice kernel, one CTA
+    per tile and as the work queue, against the oracle; the two schedules agree
+    bit for bit."""
+    monkeypatch.setenv("FPM_B200_QUAD", "1")
     monkeypatch.setenv("FPM_B200_BANDS", "1")
     cfg = gpu_cfg(led_scan_rows=7, led_scan_cols=7, tile_overlap=8)
     fs, ofs, seq, _ = dataset(cfg, fov=120, seed=31)
@@ -221,15 +224,15 @@ def test_warp_kernel_multi_tile_batch(orc, eng, monkeypatch, queue):
         assert amp < FINAL_TOL and ph < FINAL_TOL, (i, amp, ph)
 
 
-def test_warp_kernel_agrees_with_lattice_kernel(eng, monkeypatch):
-    """The two n = 64 kernels compute the same reconstruction (different FFT
-    factorisations: equal to FP32 rounding)."""
+def test_quad_kernel_agrees_with_pair_kernel(eng, monkeypatch):
+    """The two n = 64 kernels compute the same reconstruction (different lane
+    splits of the same factorisation: equal to FP32 rounding)."""
     cfg = gpu_cfg(led_scan_rows=9, led_scan_cols=9, tile_overlap=8)
     fs, _, seq, _ = dataset(cfg, fov=120, seed=33)
     opt = fpm.RunOptions(iters=2, mode="epry", tile_defocus_um=[3.0, -2.0, 0.0, 5.0])
-    monkeypatch.setenv("FPM_B200_W64", "0")
+    monkeypatch.setenv("FPM_B200_QUAD", "0")
     a = fpm.run_offline(fs, cfg, seq, opt, engine=fpm.Engine(0), stitch=False)
-    monkeypatch.setenv("FPM_B200_W64", "1")
+    monkeypatch.setenv("FPM_B200_QUAD", "1")
     b = fpm.run_offline(fs, cfg, seq, opt, engine=fpm.Engine(0), stitch=False)
     for i in range(4):
         assert rel_l2(b.tiles[i], a.tiles[i]) < 1e-5

@@ -52,11 +52,11 @@ def test_online_raster_waits_for_seed(eng):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,w64", [(64, "0"), (64, "1"), (128, "")])
-def test_online_epry_equals_offline(eng, monkeypatch, n, w64):
-    """The EPRY extension, the n = 64 warp kernel and the general-n kernel
-    through the streaming path (slot ranges, accumulated residuals)."""
-    monkeypatch.setenv("FPM_B200_W64", w64)
+@pytest.mark.parametrize("n,quad", [(64, "0"), (64, "1"), (128, "")])
+def test_online_epry_equals_offline(eng, monkeypatch, n, quad):
+    """The EPRY extension, both n = 64 kernels (pair and quad lattice) and the
+    general-n kernel through the streaming path (slot ranges, accumulated residuals)."""
+    monkeypatch.setenv("FPM_B200_QUAD", quad)
     cfg = fpm.OpticalConfig(tile_size=n, tile_overlap=8, upsample=4, led_scan_rows=7, led_scan_cols=7)
     fs, _, seq, _ = dataset(cfg, fov=2 * n - 8 if n == 64 else n, seed=36, defocus_um=8.0)
     T = len(fpm.partition_tiles(fs.width(), fs.height(), cfg))
