@@ -102,7 +102,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// 3-D map over the LR stack [F][H][pitch] u16 with a 64x64x1 box, 128B swizzle.
+// 3-D map over the LR stack [F][H][pitch] u16 with a 64x64x1 box (layout: FPM_MEAS_SWIZZLE).
 CUtensorMap encode_frames_map(const uint16_t* frames, int F, int H, int W, int64_t pitch) {
     if ((pitch * 2) % 16 != 0) throw DataError("frame row pitch must be a multiple of 8 elements");
     if (reinterpret_cast<uintptr_t>(frames) % 16 != 0) throw DataError("frame base must be 16-byte aligned");
@@ -113,7 +113,8 @@ CUtensorMap encode_frames_map(const uint16_t* frames, int F, int H, int W, int64
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t*>(frames), dims,
                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      FPM_MEAS_SWIZZLE ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
     return m;

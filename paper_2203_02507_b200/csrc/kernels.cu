@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "fft_device.cuh"
 #include "kernels.cuh"
@@ -457,8 +458,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                     const int b = 2 * u + h;
                     float Iv;
                     if (MEAS == kMeasTMA) {
-                        // 128B swizzle: 16-byte chunk b of row i sits at chunk b ^ (i & 7), i & 7 == tr
-                        const uint32_t Iu = I_s[(tr + 8 * a) * 64 + ((b ^ tr) << 3) + tc];
+                        // FPM_MEAS_SWIZZLE: 16-byte chunk b of row i sits at chunk b ^ (i & 7), i & 7 == tr
+                        const uint32_t Iu = I_s[(tr + 8 * a) * 64 + ((FPM_MEAS_SWIZZLE ? b ^ tr : b) << 3) + tc];
                         if (first) den_u += Iu;
                         Iv = float(Iu);
                     } else {
@@ -540,8 +541,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
             if (MODE == kModeEPRY) {
                 const float om = fmaxf(fmaxf(rg[8], rg[9]), fmaxf(rg[10], rg[11]));
                 const float pm = fmaxf(fmaxf(rg[12], rg[13]), fmaxf(rg[14], rg[15]));
-                inv_omax = (om > 0.f && bright) ? args.beta / om : 0.f;  // bright-field pupil steps only
-                inv_pmax = pm > 0.f ? args.alpha / pm : 0.f;
+                inv_omax = (om > 0.f && bright) ? __fdividef(args.beta, om) : 0.f;  // bright-field pupil steps only
+                inv_pmax = pm > 0.f ? __fdividef(args.alpha, pm) : 0.f;
             }
             }
 
@@ -556,6 +557,10 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                 pupil_dirty = upd_p;
                 if constexpr (FPM_O_STAGE && MODE == kModeEPRY && PRUNE && G == 1 && MEAS == kMeasTMA)
                     asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own slots
+                // dark-field updates (the large majority) take no pupil step: a block-uniform
+                // branch into a scatter without the pupil arithmetic
+                auto epry_scatter = [&](auto upd_p_tag) {
+                constexpr bool kUpdP = decltype(upd_p_tag)::value;
 #pragma unroll
                 for (int c0 = 0; c0 < NP; c0 += 8) {
                     float2 Ov[8];
@@ -577,9 +582,15 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                         const float2 d = csub(v[Lat::a(qq)][Lat::j(qq)], cmul(O, P));
                         if (on && upd_o)
                             cv[Lat::a(qq) * 8 * N + 16 * Lat::j(qq)] = cadd(O, cscale(cmulc(d, P), inv_pmax));
-                        if (on && upd_p) P_s[qq * kGroupThreads + tl] = cadd(P, cscale(cmulc(d, O), inv_omax));
+                        if constexpr (kUpdP)
+                            if (on) P_s[qq * kGroupThreads + tl] = cadd(P, cscale(cmulc(d, O), inv_omax));
                     }
                 }
+                };
+                if (upd_p)
+                    epry_scatter(std::true_type{});
+                else
+                    epry_scatter(std::false_type{});
             }
         }
         __syncthreads();  // slot barrier: canvas writes visible to the next update's gather

@@ -8,6 +8,14 @@
 namespace fpmk {
 
 enum { kModeGS = 0, kModeEPRY = 1 };
+
+// Layout of the TMA-staged 64 x 64 u16 measurement crop (n = 64 loop kernels):
+// 1 = 128B swizzle (16-byte chunk c of row r at chunk c ^ (r & 7)), 0 = row-major.
+// Row-major: every read of a thread's 32 pixels is an immediate offset from one
+// per-thread base, with the same 2-way bank pattern as the swizzled reads.
+#ifndef FPM_MEAS_SWIZZLE
+#define FPM_MEAS_SWIZZLE 0
+#endif
 enum { kMeasTMA = 0, kMeasF32 = 1 };
 
 // Per-tile LED loop (K1 fused update + K4 persistent loop). One CTA per tile,

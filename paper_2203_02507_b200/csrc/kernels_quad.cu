@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int r = tr + 8 * (2 * i + hr), cb = 2 * j + hc;
-                const uint32_t Iu = I_s[r * 64 + ((cb ^ tr) << 3) + tc];  // 128B swizzle: chunk cb ^ (r & 7)
+                const uint32_t Iu = I_s[r * 64 + ((FPM_MEAS_SWIZZLE ? cb ^ tr : cb) << 3) + tc];  // kernels.cuh
                 if (first) den_u += Iu;
                 const float Iv = float(Iu);
                 const float meas = sqrt_ftz(Iv);
