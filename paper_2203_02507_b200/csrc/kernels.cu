@@ -43,14 +43,17 @@ constexpr int kIBytes = 64 * 64 * 2;            // staged u16 measurement, TMA 1
 constexpr int kTBytes = 64 * 64 * 8;            // transpose buffer (swizzled, unpadded)
 constexpr int kGroupBytes = kIBytes + kTBytes;  // 40 KB, a multiple of 1 KB
 constexpr int kGroupThreads = 128;
-#ifndef FPM_PASS_UNROLL
-#define FPM_PASS_UNROLL 1  // two specialised FFT bodies (pruning resolved at compile time); 0: one rolled body
-#endif
 #ifndef FPM_PAIR_ROT
 #define FPM_PAIR_ROT 1  // step-1 pair twiddles W8^1, W8^3 as rotations (scale folded into the column twiddles)
 #endif
 #ifndef FPM_O_STAGE
-#define FPM_O_STAGE 1  // EPRY scatter: old canvas values staged by cp.async into the measurement buffer
+// EPRY scatter: 1 = old canvas values staged by cp.async into the measurement buffer after
+// pass 1's transpose barrier (the next crop's TMA then waits for the next update); 0 = read
+// at the scatter, the next crop's TMA issued at that barrier (measured 31.74 vs 31.17 ms)
+#define FPM_O_STAGE 0
+#endif
+#ifndef FPM_O_EARLY
+#define FPM_O_EARLY 0  // 1: the scatter's old canvas values loaded before pass 1's step 2 (measured 31.24 vs 31.16 ms)
 #endif
 #ifndef FPM_MOD_SEL
 #define FPM_MOD_SEL 0  // |e| = 0 rule by selects (1; measured +1.5%) or by a 2^-60 nudge of Re (0)
@@ -82,13 +85,25 @@ __device__ __forceinline__ int tswz(int pp) {
 }
 
 // One forward transform serves both directions (IFFT(x) = conj(FFT(conj x)), the
-// conjugations folded into gather and modulus). The update loop instantiates it
-// once per pass (FPM_PASS_UNROLL, measured 2% faster than one rolled body), so
-// the prunings resolve at compile time: skip_cols drops the zero columns of the
-// disk-limited input (IFFT), skip_rows the rows the scatter never reads (FFT).
-__device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, const float4* W4_s, int p, int h,
-                                                float sg, const float2 (&tw)[4], const float2 (&twsw)[4], float kh,
-                                                float c1, float c3, int g, bool skip_cols, bool skip_rows) {
+// conjugations folded into gather and modulus), split at the transpose: fft_first
+// (step 1, twiddle, transpose write) and fft_second (transpose read, step 2), the
+// group barrier between them issued by the caller. The update runs each half once
+// per pass with the prunings resolved at compile time: skip_cols drops the zero
+// columns of the disk-limited input (IFFT), skip_rows the rows the scatter never
+// reads (FFT).
+//
+// Transpose layouts (one swizzle tswz for both): pass 0 uses layout A — element
+// k0 = (a, 4h + m) of residue p at physical row p' = 8a + 4h + m, column p; pass 1
+// uses layout B — the same element at physical row p, column p'. A thread's layout-B
+// writes land in its own physical row, in the half (bit 2 of the column) that only
+// it read in layout A, and its layout-A writes of the next update land in the
+// column half only it read in layout B: no write can overtake another thread's
+// pending read, so the transposes need only their write-to-read barriers (the
+// barrier after the modulus is gone; the modulus's reductions and the measurement
+// buffer are released by pass 1's transpose barrier).
+__device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const float4* W4_s, int p, int h,
+                                          float sg, const float2 (&tw)[4], const float2 (&twsw)[4], float kh,
+                                          float c1, float c3, bool skip_cols, bool layout_b) {
     const int tr = p >> 3, tc = p & 7;
     // step 1: DFT8 over n1r (registers), then the pair DFT over n1c (DIT). Pruned IFFT
     // (skip_cols): only rows a in [2, 6) of columns j in {1, 2} hold data, and the
@@ -145,29 +160,65 @@ __device__ __forceinline__ void fft64x64_fwd_rt(float2 (&v)[8][4], float2* T_s, 
 #pragma unroll
         for (int a = 0; a < 8; ++a) v[a][m] = cmul_sw(v[a][m], make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
-    // transpose: element k0 = (a, 4h + m) of residue p goes to row p' = 8a + 4h + m, slot p
+    if (!layout_b) {
+        // layout A: element k0 = (a, 4h + m) of residue p goes to row p' = 8a + 4h + m, slot p
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        const int gm = ((m & 1) << 1) | (((((m >> 1) & 1) ^ h)) << 3);  // tswz(8a + 4h + m)
-        float2* wrow = T_s + (4 * h + m) * 64 + (p ^ gm);
+        for (int m = 0; m < 4; ++m) {
+            const int gm = ((m & 1) << 1) | (((((m >> 1) & 1) ^ h)) << 3);  // tswz(8a + 4h + m)
+            float2* wrow = T_s + (4 * h + m) * 64 + (p ^ gm);
 #pragma unroll
-        for (int a = 0; a < 8; ++a) wrow[a * 512] = v[a][m];
+            for (int a = 0; a < 8; ++a) wrow[a * 512] = v[a][m];
+        }
+    } else {
+        // layout B: own row p, columns (8a + 4h + m) ^ tswz(p) (128-bit stores of the pairs m,
+        // m + 1). tswz flips column bit 3 (a's parity) by g3 and bit 1 (m) by g1: four bases,
+        // the rest immediate offsets
+        const int gp = tswz(p), g3 = (gp >> 3) & 1, g1 = (gp >> 1) & 1;
+        float2* e0 = T_s + p * 64 + 8 * g3 + 4 * h + 2 * g1;  // even a, m = 0
+        float2* e2 = e0 + 2 - 4 * g1;                          // even a, m = 2
+        float2* o0 = e0 + 8 - 16 * g3;                         // odd a, m = 0
+        float2* o2 = e2 + 8 - 16 * g3;                         // odd a, m = 2
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            *reinterpret_cast<float4*>(e0 + 16 * k) = make_float4(v[2 * k][0].x, v[2 * k][0].y, v[2 * k][1].x, v[2 * k][1].y);
+            *reinterpret_cast<float4*>(e2 + 16 * k) = make_float4(v[2 * k][2].x, v[2 * k][2].y, v[2 * k][3].x, v[2 * k][3].y);
+            *reinterpret_cast<float4*>(o0 + 16 * k) =
+                make_float4(v[2 * k + 1][0].x, v[2 * k + 1][0].y, v[2 * k + 1][1].x, v[2 * k + 1][1].y);
+            *reinterpret_cast<float4*>(o2 + 16 * k) =
+                make_float4(v[2 * k + 1][2].x, v[2 * k + 1][2].y, v[2 * k + 1][3].x, v[2 * k + 1][3].y);
+        }
     }
-    group_sync(g);
-    // read row p: slots n0r * 8 + 4h + i, XOR-swizzled (bit 3 flips the row parity, bit 1 the pair)
-    const int gp = tswz(p);
-    const float2* rrow = T_s + p * 64;
-    const int ofs = (4 * h) ^ (gp & 2);
-    const int rflip = gp & 8;
+}
+
+__device__ __forceinline__ void fft_second(float2 (&v)[8][4], const float2* T_s, int p, int h, float sg,
+                                           const float2 (&tw)[4], const float2 (&twsw)[4], bool skip_rows,
+                                           bool layout_b) {
+    if (!layout_b) {
+        // layout A, read row p: slots n0r * 8 + 4h + i, XOR-swizzled (bit 3 flips the row parity,
+        // bit 1 the pair)
+        const int gp = tswz(p);
+        const float2* rrow = T_s + p * 64;
+        const int ofs = (4 * h) ^ (gp & 2);
+        const int rflip = gp & 8;
 #pragma unroll
-    for (int n0r = 0; n0r < 8; ++n0r) {
-        const float2* r = rrow + ((n0r * 8) ^ rflip) + ofs;
-        const float4 q0 = *reinterpret_cast<const float4*>(r);
-        const float4 q1 = *reinterpret_cast<const float4*>(r + (2 ^ (gp & 2)) - (gp & 2));
-        v[n0r][0] = make_float2(q0.x, q0.y);
-        v[n0r][1] = make_float2(q0.z, q0.w);
-        v[n0r][2] = make_float2(q1.x, q1.y);
-        v[n0r][3] = make_float2(q1.z, q1.w);
+        for (int n0r = 0; n0r < 8; ++n0r) {
+            const float2* r = rrow + ((n0r * 8) ^ rflip) + ofs;
+            const float4 q0 = *reinterpret_cast<const float4*>(r);
+            const float4 q1 = *reinterpret_cast<const float4*>(r + (2 ^ (gp & 2)) - (gp & 2));
+            v[n0r][0] = make_float2(q0.x, q0.y);
+            v[n0r][1] = make_float2(q0.z, q0.w);
+            v[n0r][2] = make_float2(q1.x, q1.y);
+            v[n0r][3] = make_float2(q1.z, q1.w);
+        }
+    } else {
+        // layout B, read column p of rows 8 n0r + 4h + i (tswz of those rows: bit 1 = i & 1,
+        // bit 3 = (i >> 1) ^ h, independent of n0r)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2* col = T_s + (4 * h + i) * 64 + (p ^ (((i & 1) << 1) | ((((i >> 1) & 1) ^ h) << 3)));
+#pragma unroll
+            for (int n0r = 0; n0r < 8; ++n0r) v[n0r][i] = col[n0r * 512];
+        }
     }
     // step 2: DFT8 over n0r, then the pair DFT over n0c (DIF); pruned FFT (skip_rows):
     // only outputs a in [2, 6) of the DFT8 are formed
@@ -431,14 +482,9 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
             //      run as conj(FFT(conj x)); modulus replacement
             // ---- pass 1: centered forward transform of the corrected field
             float inv_omax = 0.f, inv_pmax = 0.f;
-#if FPM_PASS_UNROLL
-#pragma unroll
-#else
-#pragma unroll 1
-#endif
-            for (int pass = 0; pass < 2; ++pass) {
-            fft64x64_fwd_rt(v, T_s, W4_s, p, h, sg, tw, twsw, kh, c1, c3, g, PRUNE && pass == 0, PRUNE && pass == 1);
-            if (pass == 1) break;
+            fft_first(v, T_s, W4_s, p, h, sg, tw, twsw, kh, c1, c3, PRUNE, false);
+            group_sync(g);
+            fft_second(v, T_s, p, h, sg, tw, twsw, false, false);
 
             // ---- modulus replacement with sqrt(I) and residual sums (recon.cpp:115-124):
             // e' = e sqrt(I)/|e| (sqrt(I) + 0i at |e| = 0, recon.cpp:122); the residual is formed
@@ -503,10 +549,13 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                 rg[warp] = num;
                 rg[4 + warp] = den;
             }
-            group_sync(g);  // staging and transpose buffers free; reductions visible
+            // ---- pass 1: centred forward transform of the corrected field (layout-B transpose)
+            fft_first(v, T_s, W4_s, p, h, sg, tw, twsw, kh, c1, c3, false, true);
+            group_sync(g);  // pass 1's transpose written; every warp past its modulus: staging buffer free,
+                            // reductions visible
 
             // EPRY (pruned, sequential): the scatter's old canvas values go into the now-free
-            // measurement staging buffer by cp.async, their latency under pass 1; the next
+            // measurement staging buffer by cp.async, their latency under pass 1's step 2; the next
             // crop's TMA is then issued at the top of the next update
             constexpr bool kOStage = FPM_O_STAGE && MODE == kModeEPRY && PRUNE && G == 1 && MEAS == kMeasTMA;
             if constexpr (kOStage) {
@@ -544,7 +593,14 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                 inv_omax = (om > 0.f && bright) ? __fdividef(args.beta, om) : 0.f;  // bright-field pupil steps only
                 inv_pmax = pm > 0.f ? __fdividef(args.alpha, pm) : 0.f;
             }
+            // EPRY: the scatter's old canvas values, loaded under pass 1's step 2
+            constexpr bool kOEarly = !FPM_O_STAGE && FPM_O_EARLY && MODE == kModeEPRY && PRUNE;
+            float2 Oe[kOEarly ? NP : 1];
+            if constexpr (kOEarly) {
+#pragma unroll
+                for (int q = 0; q < NP; ++q) Oe[q] = cv[Lat::a(q) * 8 * N + 16 * Lat::j(q)];
             }
+            fft_second(v, T_s, p, h, sg, tw, twsw, PRUNE, true);
 
             // ---- scatter into the canvas disk (recon.cpp:127-130) / EPRY update
             if (MODE == kModeGS) {
@@ -568,6 +624,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                     for (int q = 0; q < 8; ++q) {
                         if constexpr (FPM_O_STAGE && MODE == kModeEPRY && PRUNE && G == 1 && MEAS == kMeasTMA)
                             Ov[q] = reinterpret_cast<const float2*>(I_s)[(c0 + q) * kGroupThreads + tl];
+                        else if constexpr (kOEarly)
+                            Ov[q] = Oe[c0 + q];
                         else
                             Ov[q] = cv[Lat::a(c0 + q) * 8 * N + 16 * Lat::j(c0 + q)];
                     }
