@@ -278,6 +278,12 @@ struct fpmgpu_plan {
     int x_min = 0, y_min = 0;
     DevBuf<long long> out_off;
     long long out_off_pitch = -1;
+    // N = 256 canvas box: every update touches only rows / columns [cbox0, cbox0 + cboxn)
+    // (origins + support box), so init_canvas and canvas_to_field prune to it
+    int cbox0 = 0, cboxn = 0;
+    DevBuf<float2> canvas0;          // [T][cboxn][cboxn] init spectrum over the box
+    const uint16_t* seed_frame = nullptr;  // the last prologue's seed frame (the epilogue re-reads it)
+    int64_t seed_pitch = 0;
     // phase events of recent executes: [slot][4] = start, after init, after loop, after finalize
     static constexpr int kEventSlots = 256;
     std::vector<cudaEvent_t> events;
@@ -373,6 +379,40 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
             throw Unsupported("pupil disk wider than the pruned lattice needs canvas side 256 in this build");
     }
 
+    {
+        // canvas rows / columns any update reads or writes: origin + the block rows / columns
+        // the loop kernel touches — the support's range for the box and cluster kernels (they
+        // mask by support run), the lattice's [16, 48) or [0, 64) for the n = 64 lattice kernels
+        // (their gathers read every lattice position of the pruned block)
+        int s0 = p.n, s1 = 0;
+        if (!p.use_box && !p.cl) {
+            s0 = p.prune ? 16 : 0;
+            s1 = p.prune ? 48 : 64;
+        } else {
+            for (int i = 0; i < p.n; ++i)
+                for (int j = 0; j < p.n; ++j)
+                    if (sup[size_t(i) * p.n + j]) {
+                        s0 = std::min(s0, std::min(i, j));
+                        s1 = std::max(s1, std::max(i, j) + 1);
+                    }
+        }
+        int lo = p.N, hi = 0;
+        for (const short2& o : org) {
+            lo = std::min(lo, std::min(int(o.x), int(o.y)) + s0);
+            hi = std::max(hi, std::max(int(o.x), int(o.y)) + s1);
+        }
+        lo = lo / 16 * 16;
+        hi = std::min(p.N, (hi + 15) / 16 * 16);
+        const char* e = std::getenv("FPM_B200_CANVAS_BOX");
+        const bool on = !(e && e[0] == '0');
+        p.cbox0 = 0;
+        p.cboxn = 0;
+        if (on && p.N == 256 && hi > lo && (hi - lo) * 4 <= p.N * 3) {  // worth it below 3/4 of the side
+            p.cbox0 = lo;
+            p.cboxn = hi - lo;
+        }
+    }
+
     // pipelined schedule (parallel.cpp:52-111): one lag for the whole batch,
     // the largest per-tile minimum, so every tile stays sequential-equivalent
     std::vector<int2> slots;
@@ -444,6 +484,7 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
     if (p.has_pupils)
         p.pupils_init.upload(reinterpret_cast<const float2*>(r.pupils), size_t(p.T) * p.n * p.n, s);
     p.canvas.ensure(size_t(p.T) * p.N * p.N);
+    if (p.cboxn) p.canvas0.ensure(size_t(p.T) * p.cboxn * p.cboxn);
     p.pupils.ensure(size_t(p.T) * p.n * p.n);
     p.resid.ensure(size_t(p.T) * r.iters);
     p.ctx->twiddle_table(p.N);
@@ -477,6 +518,17 @@ void plan_prologue(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, cudaSt
     la.src = p.canvas.p;
     la.dst = p.canvas.p;
     la.scale = 1.0f;
+    p.seed_frame = la.frame;
+    p.seed_pitch = pitch;
+    if (p.cboxn) {  // the spectrum over the canvas box only (kernels.cuh, LinesArgs)
+        la.box0 = p.cbox0;
+        la.boxn = p.cboxn;
+        la.canvas0 = p.canvas0.p;
+        ck(fpmk::launch_lines_box(0, la, p.T, s), "init rows (box)");
+        la.scale = float(1.0 / (double(r.cfg.upsample) * r.cfg.upsample));
+        ck(fpmk::launch_lines_box(1, la, p.T, s), "init cols (box)");
+        return;
+    }
     ck(fpmk::launch_lines(0, p.N, la, p.T, s), "init rows");
     la.scale = float(1.0 / (double(r.cfg.upsample) * r.cfg.upsample));
     ck(fpmk::launch_lines(1, p.N, la, p.T, s), "init cols");
@@ -575,11 +627,23 @@ void plan_epilogue(fpmgpu_plan& p, float* hr, float* pupils_out, cudaStream_t s,
     la.scale = 1.0f;
     const long long* off = la.out_off;
     la.out_off = nullptr;
-    ck(fpmk::launch_lines(2, p.N, la, p.T, s), "final rows");
+    if (p.cboxn) {  // field = U + up^2 ifft2(canvas - canvas0), the difference confined to the box
+        la.box0 = p.cbox0;
+        la.boxn = p.cboxn;
+        la.canvas0 = p.canvas0.p;
+        la.frame = p.seed_frame;
+        la.pitch = p.seed_pitch;
+        ck(fpmk::launch_lines_box(2, la, p.T, s), "final rows (box)");
+    } else {
+        ck(fpmk::launch_lines(2, p.N, la, p.T, s), "final rows");
+    }
     la.out_off = off;
     la.dst = hr ? reinterpret_cast<float2*>(hr) : p.canvas.p;
     la.scale = float(double(r.cfg.upsample) * r.cfg.upsample / (double(p.N) * p.N));
-    ck(fpmk::launch_lines(3, p.N, la, p.T, s), "final cols");
+    if (p.cboxn)
+        ck(fpmk::launch_lines_box(3, la, p.T, s), "final cols (box)");
+    else
+        ck(fpmk::launch_lines(3, p.N, la, p.T, s), "final cols");
     if (pupils_out)
         ck(cudaMemcpyAsync(pupils_out, p.pupils.p, sizeof(float2) * size_t(p.T) * p.n * p.n,
                            cudaMemcpyDeviceToDevice, s), "pupil out");
@@ -616,7 +680,9 @@ bool same_request(const HostSlot& c, const fpmgpu_recon_request& r, std::vector<
     // kernel-selection overrides change the plans too
     const char* cl_env = std::getenv("FPM_B200_CLUSTER");
     const char* q_env = std::getenv("FPM_B200_QUAD");
-    ki.insert(ki.end(), {box_forced() ? 1 : 0, cl_env ? std::atoi(cl_env) : -1, q_env && q_env[0] ? q_env[0] : -1});
+    const char* b_env = std::getenv("FPM_B200_CANVAS_BOX");
+    ki.insert(ki.end(), {box_forced() ? 1 : 0, cl_env ? std::atoi(cl_env) : -1, q_env && q_env[0] ? q_env[0] : -1,
+                         b_env && b_env[0] ? b_env[0] : -1});
     kd.push_back(r.alpha);
     kd.push_back(r.beta);
     if (r.tile_defocus_um) kd.insert(kd.end(), r.tile_defocus_um, r.tile_defocus_um + r.num_tiles);

@@ -62,6 +62,12 @@ struct LinesArgs {
     // mosaic) when the tiles abut without overlap; nullptr = dst[t][N][N]
     const long long* out_off;
     long long out_pitch;
+    // N = 256 canvas box (launch_lines_box): the LED loop only ever touches rows and
+    // columns [box0, box0 + boxn) of a canvas, so init_canvas forms the spectrum there
+    // only and canvas_to_field transforms only the change there:
+    // field = U + up^2 ifft2(canvas - canvas0), U = bilinear(sqrt(seed crop))
+    int box0, boxn;
+    float2* canvas0;          // [T][boxn][boxn] init spectrum over the box
 };
 
 // General tile sides (n = 64, 128, 256): warp-FFT row/column passes over the
@@ -123,6 +129,8 @@ cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorM
                           const LoopArgs& a, int T, cudaStream_t s);
 // which: 0 init rows (frame -> canvas), 1 init cols, 2 finalize rows, 3 finalize cols
 cudaError_t launch_lines(int which, int N, const LinesArgs& a, int T, cudaStream_t s);
+// the box-pruned passes for N = 256 (a.box0, a.boxn multiples of 16; which as above)
+cudaError_t launch_lines_box(int which, const LinesArgs& a, int T, cudaStream_t s);
 cudaError_t launch_build_pupils(float2* pupils, const uint8_t* support, const double* defocus,
                                 int n, int T, double dk, double inv_l2, cudaStream_t s);
 

@@ -248,6 +248,161 @@ __global__ void __launch_bounds__(512) lines_fft_w256(const LinesArgs a) {
     }
 }
 
+// Box-pruned N = 256 passes (see LinesArgs): the same warp FFT and staging as
+// lines_fft_w256, over fewer lines and with zero / skipped ranges:
+//   0 init rows:  all 256 rows of bilinear(sqrt(seed)) * C -> FFT -> box columns only
+//   1 init cols:  box columns, all rows -> FFT -> box rows * C / up^2 -> canvas and canvas0
+//   2 final rows: box rows, input (canvas - canvas0) * C on box columns, 0 elsewhere -> IFFT
+//                 -> the whole row back into the canvas
+//   3 final cols: all columns, input the box rows (0 elsewhere) -> IFFT -> * C up^2 / N^2
+//                 + bilinear(sqrt(seed)) -> dst (or the mosaic via out_off)
+__device__ __forceinline__ float seed_bilinear(const LinesArgs& a, int tile, int i, int j) {
+    const int n = a.n;
+    const float fy = (i + 0.5f) / a.up - 0.5f, fx = (j + 0.5f) / a.up - 0.5f;
+    int ya = int(floorf(fy)), xa = int(floorf(fx));
+    const float wy = fy - ya, wx = fx - xa;
+    const int yb = min(ya + 1, n - 1), xb = min(xa + 1, n - 1);
+    ya = max(ya, 0);
+    xa = max(xa, 0);
+    const int2 txy = a.tile_xy[tile];
+    const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
+    const float v00 = sqrtf(float(f[size_t(ya) * a.pitch + xa]));
+    const float v01 = sqrtf(float(f[size_t(ya) * a.pitch + xb]));
+    const float v10 = sqrtf(float(f[size_t(yb) * a.pitch + xa]));
+    const float v11 = sqrtf(float(f[size_t(yb) * a.pitch + xb]));
+    return (1.f - wy) * ((1.f - wx) * v00 + wx * v01) + wy * ((1.f - wx) * v10 + wx * v11);
+}
+
+template <int WHICH>
+__global__ void __launch_bounds__(512) lines_box_w256(const LinesArgs a) {
+    constexpr int NL = 256, LPB = 16, M = 8, LS = NL + NL / 32;
+    constexpr bool INV = WHICH >= 2;
+    constexpr bool COLS = (WHICH & 1) == 1;
+    __shared__ float2 s[LPB * LS];
+    const int tile = blockIdx.y;
+    const int b0 = a.box0, bn = a.boxn;
+    const int l0 = (WHICH == 1 || WHICH == 2 ? b0 : 0) + blockIdx.x * LPB;  // first line of the block
+    const size_t base = size_t(tile) * NL * NL;
+    float2* c0 = a.canvas0 + size_t(tile) * bn * bn;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    auto pad = [](int i) { return i + (i >> 5); };
+    auto in_box = [&](int x) { return x >= b0 && x < b0 + bn; };
+    // sqrt of the seed-crop window the block's bilinear samples read (init rows: <= 6 LR rows
+    // x n columns; final cols: n rows x <= 6 LR columns), staged once
+    constexpr int kSq = 1536;
+    __shared__ float sq[(WHICH == 0 || WHICH == 3) ? kSq : 1];
+    int wy0 = 0, wx0 = 0, wsw = 0;
+    bool sq_on = false;
+    auto lr_lo = [&](int hr0) { return max(int(floorf((hr0 + 0.5f) / a.up - 0.5f)), 0); };
+    auto lr_hi = [&](int hr1) { return min(int(floorf((hr1 + 0.5f) / a.up - 0.5f)) + 1, a.n - 1); };
+    if (WHICH == 0 || WHICH == 3) {
+        const int n = a.n;
+        int wy1, wx1;
+        if (WHICH == 0) {
+            wy0 = lr_lo(l0);
+            wy1 = lr_hi(l0 + LPB - 1);
+            wx0 = 0;
+            wx1 = n - 1;
+        } else {
+            wy0 = 0;
+            wy1 = n - 1;
+            wx0 = lr_lo(l0);
+            wx1 = lr_hi(l0 + LPB - 1);
+        }
+        wsw = wx1 - wx0 + 1;
+        sq_on = (wy1 - wy0 + 1) * wsw <= kSq;
+        if (sq_on) {
+            const int2 txy = a.tile_xy[tile];
+            const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
+            for (int k = threadIdx.x; k < (wy1 - wy0 + 1) * wsw; k += blockDim.x) {
+                const int r = k / wsw, c = k - r * wsw;
+                sq[k] = sqrtf(float(f[size_t(wy0 + r) * a.pitch + wx0 + c]));
+            }
+        }
+        __syncthreads();
+    }
+    auto bilinear = [&](int i, int j) -> float {  // upsample_bilinear (field.cpp:89-112)
+        if (!sq_on) return seed_bilinear(a, tile, i, j);
+        const int n = a.n;
+        const float fy = (i + 0.5f) / a.up - 0.5f, fx = (j + 0.5f) / a.up - 0.5f;
+        int ya = int(floorf(fy)), xa = int(floorf(fx));
+        const float wy = fy - ya, wx = fx - xa;
+        const int yb = min(ya + 1, n - 1), xb = min(xa + 1, n - 1);
+        ya = max(ya, 0);
+        xa = max(xa, 0);
+        const float* q0 = sq + (ya - wy0) * wsw - wx0;
+        const float* q1 = sq + (yb - wy0) * wsw - wx0;
+        return (1.f - wy) * ((1.f - wx) * q0[xa] + wx * q0[xb]) + wy * ((1.f - wx) * q1[xa] + wx * q1[xb]);
+    };
+    for (int idx = threadIdx.x; idx < LPB * NL; idx += blockDim.x) {
+        int line, e;
+        if (COLS) {
+            e = idx / LPB;
+            line = idx - e * LPB;
+        } else {
+            line = idx / NL;
+            e = idx - line * NL;
+        }
+        float2 x = make_float2(0.f, 0.f);
+        if (WHICH == 0) {
+            const int i = l0 + line, j = e;
+            const float val = bilinear(i, j);
+            x = make_float2(((i + j) & 1) ? -val : val, 0.f);
+        } else if (WHICH == 1) {
+            x = a.src[base + size_t(e) * NL + l0 + line];
+        } else if (WHICH == 2) {
+            const int i = l0 + line;
+            if (in_box(e)) {
+                x = csub(a.src[base + size_t(i) * NL + e], c0[size_t(i - b0) * bn + (e - b0)]);
+                if ((i + e) & 1) x = cneg(x);
+            }
+        } else {
+            if (in_box(e)) x = a.src[base + size_t(e) * NL + l0 + line];
+        }
+        if (INV) x.y = -x.y;
+        s[line * LS + pad(e)] = x;
+    }
+    __syncthreads();
+    {
+        WarpFFT<M> F;
+        F.init_table(l, NL, a.tw);
+        float2* ln = s + w * LS;
+        float2 x[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) x[m] = ln[pad(l + 32 * m)];
+        F.f1(x);
+#pragma unroll
+        for (int k0 = 0; k0 < M; ++k0) ln[pad(k0 + M * brev5(l))] = x[k0];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < LPB * NL; idx += blockDim.x) {
+        if (COLS) {
+            const int e = idx / LPB, line = idx - e * LPB;
+            const int i = e, j = l0 + line;
+            if (WHICH == 1 && !in_box(i)) continue;
+            float2 x = s[line * LS + pad(e)];
+            if (INV) x.y = -x.y;
+            const float sc = ((i + j) & 1) ? -a.scale : a.scale;
+            x = cscale(x, sc);
+            if (WHICH == 1) {
+                a.dst[base + size_t(i) * NL + j] = x;
+                c0[size_t(i - b0) * bn + (j - b0)] = x;
+            } else {
+                x.x += bilinear(i, j);
+                const size_t o = a.out_off ? size_t(a.out_off[tile]) + size_t(i) * a.out_pitch + j
+                                           : base + size_t(i) * NL + j;
+                a.dst[o] = x;
+            }
+        } else {
+            const int line = idx / NL, e = idx - line * NL;
+            if (WHICH == 0 && !in_box(e)) continue;
+            float2 x = s[line * LS + pad(e)];
+            if (INV) x.y = -x.y;
+            a.dst[base + size_t(l0 + line) * NL + e] = x;
+        }
+    }
+}
+
 template <int NL, int LPB, int WHICH>
 cudaError_t launch_lines_t(const LinesArgs& a, int T, cudaStream_t s) {
     const size_t smem = size_t(2) * LPB * NL * sizeof(float2);
@@ -319,6 +474,20 @@ cudaError_t launch_lines(int which, int N, const LinesArgs& a, int T, cudaStream
         case 1024: return launch_lines_n<1024, 4>(which, a, T, s);
     }
     return cudaErrorNotSupported;  // no line-FFT instantiation for this side
+}
+
+cudaError_t launch_lines_box(int which, const LinesArgs& a, int T, cudaStream_t s) {
+    if (a.boxn <= 0 || a.boxn % 16 || a.box0 % 16 || a.box0 < 0 || a.box0 + a.boxn > 256) return cudaErrorInvalidValue;
+    const int blocks = (which == 1 || which == 2) ? a.boxn / 16 : 256 / 16;
+    const dim3 grid(blocks, T);
+    switch (which) {
+        case 0: lines_box_w256<0><<<grid, 512, 0, s>>>(a); break;
+        case 1: lines_box_w256<1><<<grid, 512, 0, s>>>(a); break;
+        case 2: lines_box_w256<2><<<grid, 512, 0, s>>>(a); break;
+        case 3: lines_box_w256<3><<<grid, 512, 0, s>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_build_pupils(float2* pupils, const uint8_t* support, const double* defocus, int n, int T,
