@@ -375,6 +375,33 @@ __global__ void __launch_bounds__(512) lines_box_w256(const LinesArgs a) {
         for (int k0 = 0; k0 < M; ++k0) ln[pad(k0 + M * brev5(l))] = x[k0];
     }
     __syncthreads();
+    if (WHICH == 3 && sq_on) {
+        // final cols: a thread keeps one column (its bilinear x weights) over every 32nd row
+        const int line = threadIdx.x & (LPB - 1), j = l0 + line, n = a.n;
+        const float fx = (j + 0.5f) / a.up - 0.5f;
+        int xa = int(floorf(fx));
+        const float wx = fx - xa;
+        const int xb = min(xa + 1, n - 1) - wx0;
+        xa = max(xa, 0) - wx0;
+        const size_t obase = a.out_off ? size_t(a.out_off[tile]) + j : base + j;
+        const size_t opitch = a.out_off ? size_t(a.out_pitch) : size_t(NL);
+        for (int i = threadIdx.x / LPB; i < NL; i += blockDim.x / LPB) {
+            float2 x = s[line * LS + pad(i)];
+            x.y = -x.y;
+            const float sc = ((i + j) & 1) ? -a.scale : a.scale;
+            x = cscale(x, sc);
+            const float fy = (i + 0.5f) / a.up - 0.5f;
+            int ya = int(floorf(fy));
+            const float wy = fy - ya;
+            const int yb = min(ya + 1, n - 1) - wy0;
+            ya = max(ya, 0) - wy0;
+            const float* q0 = sq + ya * wsw;
+            const float* q1 = sq + yb * wsw;
+            x.x += (1.f - wy) * ((1.f - wx) * q0[xa] + wx * q0[xb]) + wy * ((1.f - wx) * q1[xa] + wx * q1[xb]);
+            a.dst[obase + size_t(i) * opitch] = x;
+        }
+        return;
+    }
     for (int idx = threadIdx.x; idx < LPB * NL; idx += blockDim.x) {
         if (COLS) {
             const int e = idx / LPB, line = idx - e * LPB;
@@ -400,6 +427,61 @@ __global__ void __launch_bounds__(512) lines_box_w256(const LinesArgs a) {
             if (INV) x.y = -x.y;
             a.dst[base + size_t(l0 + line) * NL + e] = x;
         }
+    }
+}
+
+// Box init rows, separably: U(i, j) = (1 - wy_i) h_ya(j) + wy_i h_yb(j), h_y the
+// horizontal bilinear interpolation of sqrt(seed) LR row y, so the row spectrum
+// FFT_j(C U(i, .)) = (-1)^i [(1 - wy_i) G_ya + wy_i G_yb] with G_y = FFT_j((-1)^j h_y):
+// a block of 32 HR rows transforms the <= 10 LR rows they interpolate from (one warp
+// each) instead of 32 HR rows, and writes the box columns of its 32 rows.
+__global__ void __launch_bounds__(512) lines_box_init_rows(const LinesArgs a) {
+    constexpr int NL = 256, RB = 32, MAXLR = 16, M = 8, LS = NL + NL / 32;
+    __shared__ float2 s[MAXLR * LS];
+    const int tile = blockIdx.y, i0 = blockIdx.x * RB;
+    const int b0 = a.box0, bn = a.boxn, n = a.n, up = a.up;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    auto pad = [](int i) { return i + (i >> 5); };
+    auto lr_of = [&](int i) { return max(int(floorf((i + 0.5f) / up - 0.5f)), 0); };
+    const int y0 = lr_of(i0), y1 = min(lr_of(i0 + RB - 1) + 1, n - 1);
+    const int ny = y1 - y0 + 1;  // <= 10 for up = 4 (checked by the launcher's shape)
+    const int2 txy = a.tile_xy[tile];
+    const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
+    // h_y(j) (-1)^j for the block's LR rows
+    for (int idx = threadIdx.x; idx < ny * NL; idx += blockDim.x) {
+        const int r = idx / NL, j = idx - r * NL, y = y0 + r;
+        const float fx = (j + 0.5f) / up - 0.5f;
+        int xa = int(floorf(fx));
+        const float wx = fx - xa;
+        const int xb = min(xa + 1, n - 1);
+        xa = max(xa, 0);
+        const float v = (1.f - wx) * sqrtf(float(f[size_t(y) * a.pitch + xa])) + wx * sqrtf(float(f[size_t(y) * a.pitch + xb]));
+        s[r * LS + pad(j)] = make_float2((j & 1) ? -v : v, 0.f);
+    }
+    __syncthreads();
+    if (w < ny) {
+        WarpFFT<M> F;
+        F.init_table(l, NL, a.tw);
+        float2* ln = s + w * LS;
+        float2 x[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) x[m] = ln[pad(l + 32 * m)];
+        F.f1(x);
+#pragma unroll
+        for (int k0 = 0; k0 < M; ++k0) ln[pad(k0 + M * brev5(l))] = x[k0];
+    }
+    __syncthreads();
+    const size_t base = size_t(tile) * NL * NL;
+    for (int idx = threadIdx.x; idx < RB * bn; idx += blockDim.x) {
+        const int r = idx / bn, k = b0 + (idx - r * bn), i = i0 + r;
+        const float fy = (i + 0.5f) / up - 0.5f;
+        int ya = int(floorf(fy));
+        const float wy = fy - ya;
+        const int yb = min(ya + 1, n - 1);
+        ya = max(ya, 0);
+        const float2 ga = s[(ya - y0) * LS + pad(k)], gb = s[(yb - y0) * LS + pad(k)];
+        const float sg = (i & 1) ? -1.f : 1.f;
+        a.dst[base + size_t(i) * NL + k] = make_float2(sg * ((1.f - wy) * ga.x + wy * gb.x), sg * ((1.f - wy) * ga.y + wy * gb.y));
     }
 }
 
@@ -480,8 +562,15 @@ cudaError_t launch_lines_box(int which, const LinesArgs& a, int T, cudaStream_t 
     if (a.boxn <= 0 || a.boxn % 16 || a.box0 % 16 || a.box0 < 0 || a.box0 + a.boxn > 256) return cudaErrorInvalidValue;
     const int blocks = (which == 1 || which == 2) ? a.boxn / 16 : 256 / 16;
     const dim3 grid(blocks, T);
+    // the separable init rows need <= 16 LR rows per 32 HR rows (upsample >= 3)
+    const bool sep = a.up >= 3 && std::getenv("FPM_B200_INIT_SEP") == nullptr;
     switch (which) {
-        case 0: lines_box_w256<0><<<grid, 512, 0, s>>>(a); break;
+        case 0:
+            if (sep)
+                lines_box_init_rows<<<dim3(256 / 32, T), 512, 0, s>>>(a);
+            else
+                lines_box_w256<0><<<grid, 512, 0, s>>>(a);
+            break;
         case 1: lines_box_w256<1><<<grid, 512, 0, s>>>(a); break;
         case 2: lines_box_w256<2><<<grid, 512, 0, s>>>(a); break;
         case 3: lines_box_w256<3><<<grid, 512, 0, s>>>(a); break;
