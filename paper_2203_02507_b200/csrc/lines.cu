@@ -273,8 +273,11 @@ __device__ __forceinline__ float seed_bilinear(const LinesArgs& a, int tile, int
     return (1.f - wy) * ((1.f - wx) * v00 + wx * v01) + wy * ((1.f - wx) * v10 + wx * v11);
 }
 
+#ifndef FPM_LINES_BOX_MINB
+#define FPM_LINES_BOX_MINB 3  // resident 512-thread blocks per SM the register budget targets
+#endif
 template <int WHICH>
-__global__ void __launch_bounds__(512) lines_box_w256(const LinesArgs a) {
+__global__ void __launch_bounds__(512, FPM_LINES_BOX_MINB) lines_box_w256(const LinesArgs a) {
     constexpr int NL = 256, LPB = 16, M = 8, LS = NL + NL / 32;
     constexpr bool INV = WHICH >= 2;
     constexpr bool COLS = (WHICH & 1) == 1;
