@@ -246,11 +246,19 @@ def run_b200(args, W: Workload, rank, world):
     from paper_2203_02507_b200.distributed import (PeerMosaic, allreduce_sum, band_layout, broadcast_from_rank0,
                                                    shard_request, stitch_band)
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # collectives: NCCL on the device (the product setup); --dist-backend gloo runs the same
+    # multi-rank path with host-side collectives, e.g. several ranks sharing one GPU for a
+    # functional check of the strong-scaled step (not a measurement)
+    nccl = args.dist_backend == "nccl"
+    cdev = dev if nccl else torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if nccl:
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     cfg = workload_cfg(W)
     seq, xy_all, of_all, defocus_all = geometry(W, cfg)
@@ -281,12 +289,12 @@ def run_b200(args, W: Workload, rank, world):
     # written by every rank over NVLink (CUDA IPC) in the strong-scaled run
     mosaic = (torch.empty((lay.rows, lay.cols, 2), dtype=torch.float32, device=dev)
               if (rank == 0 or not multi) else None)
-    peer = PeerMosaic(eng, rank, mosaic.data_ptr() if mosaic is not None else None, broadcast_from_rank0(dev)) \
-        if multi else None
+    peer = PeerMosaic(eng, rank, mosaic.data_ptr() if mosaic is not None else None,
+                      broadcast_from_rank0(dev if nccl else None)) if multi else None
     mosaic_ptr = peer.ptr if multi else mosaic.data_ptr()
     band_ptr = mosaic_ptr + lay.row_lo * lay.cols * 8  # the band's top-left tile (abutting tiles)
-    token = torch.zeros(1, dtype=torch.float32, device=dev)
-    combine = allreduce_sum(dev) if multi else None
+    token = torch.zeros(1, dtype=torch.float32, device=cdev)
+    combine = allreduce_sum(dev if nccl else None) if multi else None
     stream = torch.cuda.current_stream(dev)
     share = world if strong else 1  # ranks sharing one FOV's stack
     flush = l2_flush_needed(W, share)
@@ -301,6 +309,8 @@ def run_b200(args, W: Workload, rank, world):
             stitch_band(eng, cfg, xy_all, me.tile_lo, me.tile_hi, hr.data_ptr(), mosaic_ptr, lay.cols, combine,
                         stream.cuda_stream)
         if multi:  # every band of rank 0's mosaic is written once every rank's kernels are past this point
+            if not nccl:
+                stream.synchronize()
             dist.all_reduce(token)
 
     for _ in range(args.warmup):
@@ -331,7 +341,7 @@ def run_b200(args, W: Workload, rank, world):
     assert nexec == args.steps, nexec
     ms_loop, ms_init, ms_fin = ms_loop / nexec, ms_init / nexec, ms_fin / nexec
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ok = bool(torch.isfinite(resid).all().item())
@@ -341,9 +351,9 @@ def run_b200(args, W: Workload, rank, world):
     e2e = None
     if not args.no_e2e:
         if multi:
-            e2e = e2e_strong(args, W, me, plan, lay, band_ptr, abut, mosaic, rank, world, dev)
+            e2e = e2e_strong(args, W, me, plan, lay, band_ptr, abut, mosaic, rank, world, dev, cdev)
         else:  # one GPU (or weak scaling: every rank its own FOV) through the host-buffer C-ABI call
-            e2e = e2e_leg(args, W, cfg, seq, xy_all, of_all, defocus_all, eng, world)
+            e2e = e2e_leg(args, W, cfg, seq, xy_all, of_all, defocus_all, eng, world, cdev)
 
     out = None
     if rank == 0:
@@ -423,7 +433,8 @@ def run_b200(args, W: Workload, rank, world):
     return 0
 
 
-def e2e_strong(args, W: Workload, me, plan, lay, band_ptr: int, abut: bool, mosaic, rank: int, world: int, dev):
+def e2e_strong(args, W: Workload, me, plan, lay, band_ptr: int, abut: bool, mosaic, rank: int, world: int, dev,
+               cdev):
     """BASELINE config 4 end to end: every rank uploads its band of the LR stack
     from pinned host memory, reconstructs it and writes its band of rank 0's
     mosaic over NVLink; rank 0 copies the mosaic and every rank its residuals
@@ -442,13 +453,15 @@ def e2e_strong(args, W: Workload, me, plan, lay, band_ptr: int, abut: bool, mosa
     resid = torch.empty((T, W.iters), dtype=torch.float64, device=dev)
     res_host = torch.empty((T, W.iters), dtype=torch.float64).pin_memory()
     mos_host = torch.empty(tuple(mosaic.shape), dtype=torch.float32).pin_memory() if rank == 0 else None
-    token = torch.zeros(1, dtype=torch.float32, device=dev)
+    token = torch.zeros(1, dtype=torch.float32, device=cdev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
         frames.copy_(host, non_blocking=True)
         plan.execute_mosaic(frames.data_ptr(), W.fov, band_ptr, lay.cols, resid.data_ptr(), None, stream.cuda_stream)
         res_host.copy_(resid, non_blocking=True)
+        if cdev.type == "cpu":
+            stream.synchronize()
         dist.all_reduce(token)
         if rank == 0:
             mos_host.copy_(mosaic, non_blocking=True)
@@ -461,10 +474,10 @@ def e2e_strong(args, W: Workload, me, plan, lay, band_ptr: int, abut: bool, mosa
     for _ in range(args.steps):
         step()
     wall = (time.perf_counter() - t0) / args.steps
-    t = torch.tensor([wall], dtype=torch.float64, device=dev)
+    t = torch.tensor([wall], dtype=torch.float64, device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     wall = float(t.item())
-    h2d = torch.tensor([host.numel() * 2], dtype=torch.float64, device=dev)
+    h2d = torch.tensor([host.numel() * 2], dtype=torch.float64, device=cdev)
     dist.all_reduce(h2d)
     d2h = W.tiles * W.iters * 8 + lay.rows * lay.cols * 8
     return {"value": W.updates / wall, "unit": UNIT, "ms_per_step": wall * 1000.0,
@@ -474,7 +487,7 @@ def e2e_strong(args, W: Workload, me, plan, lay, band_ptr: int, abut: bool, mosa
                     "memory; one FOV per step, wall clock, max over ranks"}
 
 
-def e2e_leg(args, W: Workload, cfg, seq, xy, of, defocus, eng, world: int = 1):
+def e2e_leg(args, W: Workload, cfg, seq, xy, of, defocus, eng, world: int = 1, cdev=None):
     """Same metric through the reference-facing host-buffer call (fpmgpu_reconstruct_tiles):
     pinned host LR stack -> H2D -> reconstruct -> D2H of HR tiles + residuals, every step.
     With N ranks (weak scaling) every rank times its own FOV; the slowest rank's wall
@@ -530,7 +543,8 @@ def e2e_leg(args, W: Workload, cfg, seq, xy, of, defocus, eng, world: int = 1):
         fn()
         wall = (time.perf_counter() - t0) / args.steps
         if world > 1:
-            t = torch.tensor([wall], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+            t = torch.tensor([wall], dtype=torch.float64,
+                             device=cdev if cdev is not None else torch.device("cuda", torch.cuda.current_device()))
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall = float(t.item())
         return wall
@@ -565,6 +579,8 @@ def main():
     ap.add_argument("--scaling", choices=["weak", "strong"], default="strong")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="collectives under torchrun (gloo: host-side, e.g. ranks sharing one GPU for a functional check)")
     args = ap.parse_args()
     if args.impl == "b200":
         args.warmup = max(args.warmup, 3)
