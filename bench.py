@@ -579,12 +579,17 @@ def main():
     ap.add_argument("--scaling", choices=["weak", "strong"], default="strong")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", choices=["gs", "epry"], default=None,
+                    help="override the workload's update rule (default: the BASELINE config's)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="collectives under torchrun (gloo: host-side, e.g. ranks sharing one GPU for a functional check)")
     args = ap.parse_args()
     if args.impl == "b200":
         args.warmup = max(args.warmup, 3)
     W = WORKLOADS[args.config]
+    if args.mode:  # e.g. config 3 in GS mode: the reference's own update rule (EPRY is an extension)
+        from dataclasses import replace
+        W = replace(W, mode=args.mode)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
