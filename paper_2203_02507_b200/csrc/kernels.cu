@@ -58,6 +58,9 @@ constexpr int kGroupThreads = 128;
 #ifndef FPM_MOD_SEL
 #define FPM_MOD_SEL 0  // |e| = 0 rule by selects (1; measured +1.5%) or by a 2^-60 nudge of Re (0)
 #endif
+#ifndef FPM_O_SMEM
+#define FPM_O_SMEM 0  // EPRY: the gathered canvas values kept in shared memory for the scatter (+8 KB per CTA)
+#endif
 #ifndef FPM_LOOP_MINB
 #define FPM_LOOP_MINB 4  // resident tiles per SM the register budget is sized for
 #endif
@@ -271,6 +274,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
     b += size_t(G) * (sizeof(uint64_t) + 16 * sizeof(float));     // mbarriers + reductions
     b += size_t(L) * (sizeof(short2) + sizeof(int) + sizeof(float) + 1);  // origins, frame map, sum(I), bright flags
     b += 8;                                                       // work-queue item (4-byte aligned)
+    if (FPM_O_SMEM) b = ((b + 15) & ~size_t(15)) + size_t(nslots) * kGroupThreads * sizeof(float2);
     return b;
 }
 
@@ -318,6 +322,9 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     off += size_t(L);
     off = (off + 3) & ~size_t(3);
     int* item_s = reinterpret_cast<int*>(smem + off);  // work queue: the CTA's current item
+    off += 8;
+    constexpr bool kOSm = FPM_O_SMEM && MODE == kModeEPRY && PRUNE && G == 1;
+    float2* O_sm = reinterpret_cast<float2*>(smem + ((off + 15) & ~size_t(15)));  // [NP][128] (kOSm)
     uint64_t* bar = bars + g;
     float* rg = red + g * 16;
 
@@ -451,6 +458,10 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
             float2 v[8][4];  // lattice positions outside the disk block are never read (pruned IFFT)
 #pragma unroll
             for (int q = 0; q < NP; ++q) v[Lat::a(q)][Lat::j(q)] = cv[Lat::a(q) * 8 * N + 16 * Lat::j(q)];
+            if constexpr (kOSm) {
+#pragma unroll
+                for (int q = 0; q < NP; ++q) O_sm[q * kGroupThreads + tl] = v[Lat::a(q)][Lat::j(q)];
+            }
             // EPRY maxima (block-uniform branches): max|O_D|^2 only for bright-field updates (the
             // only ones that take a pupil step), max|P|^2 only after the pupil changed — otherwise
             // the reduction slots keep their last values
@@ -624,6 +635,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                     for (int q = 0; q < 8; ++q) {
                         if constexpr (FPM_O_STAGE && MODE == kModeEPRY && PRUNE && G == 1 && MEAS == kMeasTMA)
                             Ov[q] = reinterpret_cast<const float2*>(I_s)[(c0 + q) * kGroupThreads + tl];
+                        else if constexpr (kOSm)
+                            Ov[q] = O_sm[(c0 + q) * kGroupThreads + tl];
                         else if constexpr (kOEarly)
                             Ov[q] = Oe[c0 + q];
                         else
