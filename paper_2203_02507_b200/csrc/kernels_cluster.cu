@@ -33,6 +33,9 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef FPM_CL_DB256
+#define FPM_CL_DB256 0  // n = 256 on 8-CTA clusters: double-buffered slabs (st.async + mbarrier, no end-of-update barrier)
+#endif
 #ifndef FPM_CL_PF8
 #define FPM_CL_PF8 0  // 1: row prefetch for n = 256 too (more registers per thread)
 #endif
@@ -54,7 +57,7 @@ __host__ __device__ static size_t row_stage_bytes(int n, int box, int nw) {
 
 size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
     const size_t sw = size_t(n / cl);
-    const size_t nbuf = n <= 128 ? 2 : 1;                  // double-buffered slabs (small n)
+    const size_t nbuf = (n <= 128 || (FPM_CL_DB256 && n == 256 && cl >= 8)) ? 2 : 1;  // double-buffered slabs
     size_t b = nbuf * size_t(box) * (sw + 1) * sizeof(float2);  // column slab(s) of the box rows
     b += sw * size_t(n) * sizeof(uint16_t);               // measurement slab
     b += size_t(n) * sizeof(short2);                      // support run per row
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
     constexpr bool PFC = M <= 4 || FPM_CL_PFC8;  // phase C: scatter operands loaded before the FFT
     // DB: two slab / reduction buffers used alternately, so an update's phase A never
     // overwrites what the previous update's phase C still reads: no end-of-update barrier
-    constexpr bool DB = NLR <= 128;
+    constexpr bool DB = NLR <= 128 || (FPM_CL_DB256 && NLR == 256 && CL >= 8);
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = int(cluster.block_rank());
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
