@@ -260,6 +260,14 @@ int fpmgpu_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset);
 int fpmgpu_ipc_open(fpmgpu_context* ctx, const void* handle, void** dev_ptr);
 int fpmgpu_ipc_close(fpmgpu_context* ctx, void* dev_ptr);
 
+/* Batched 2-D complex128 FFT, in place on data_dev [batch][rows][cols] (device,
+ * interleaved re/im doubles), sides with factors 2, 3, 5 up to 4096; forward
+ * unnormalised, inverse scaled by 1/(rows*cols) (field.cpp:18-67 before the
+ * shifts). The transforms of the GPU forward model (simulate_dataset,
+ * forward.cpp:172-282), whose tile grids are 96 / 120 / 384 / 480 ... points. */
+int fpmgpu_fft2_c128(fpmgpu_context* ctx, double* data_dev, int64_t batch, int rows, int cols,
+                     int inverse, void* stream);
+
 /* Page-locked host buffers (outputs of the async host path must be page-locked
  * for the copies to overlap; pageable outputs make the call synchronous). */
 int fpmgpu_host_alloc(int64_t bytes, void** ptr);

@@ -116,7 +116,7 @@ EXPORTS = [
     "fpmgpu_online_begin", "fpmgpu_online_push", "fpmgpu_online_finish", "fpmgpu_online_destroy",
     "fpmgpu_reconstruct_tiles_async", "fpmgpu_wait", "fpmgpu_plan_execute_mosaic", "fpmgpu_mosaic_band_layout",
     "fpmgpu_mosaic_band_sums", "fpmgpu_mosaic_band_assemble", "fpmgpu_ipc_get_handle", "fpmgpu_ipc_open",
-    "fpmgpu_ipc_close", "fpmgpu_host_alloc", "fpmgpu_host_free",
+    "fpmgpu_ipc_close", "fpmgpu_host_alloc", "fpmgpu_host_free", "fpmgpu_fft2_c128",
 ]
 
 _lib: C.CDLL | None = None
@@ -172,6 +172,7 @@ def lib() -> C.CDLL:
         L.fpmgpu_ipc_close.argtypes = [C.c_void_p, C.c_void_p]
         L.fpmgpu_host_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
         L.fpmgpu_host_free.argtypes = [C.c_void_p]
+        L.fpmgpu_fft2_c128.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]
         _lib = L
     return _lib
 

@@ -1726,6 +1726,25 @@ int fpmgpu_ipc_close(fpmgpu_context* ctx, void* dev_ptr) {
     });
 }
 
+int fpmgpu_fft2_c128(fpmgpu_context* ctx, double* data_dev, int64_t batch, int rows, int cols, int inverse,
+                     void* stream) {
+    return guarded([&] {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (batch < 0 || rows < 1 || cols < 1) throw DataError("fft2: empty or negative shape");
+        if (!fpmk::fft_c128_supported(rows) || !fpmk::fft_c128_supported(cols))
+            throw Unsupported("fft2: sides must factor into 2, 3 and 5 and be at most 4096");
+        if (batch == 0) return;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        double2* tmp = nullptr;
+        const size_t bytes = size_t(batch) * rows * cols * sizeof(double2);
+        ck(cudaMallocAsync(reinterpret_cast<void**>(&tmp), bytes, s), "cudaMallocAsync");
+        const cudaError_t e = fpmk::fft2_c128(reinterpret_cast<double2*>(data_dev), tmp, batch, rows, cols,
+                                               inverse != 0, s);
+        cudaFreeAsync(tmp, s);
+        ck(e, "fft2_c128");
+    });
+}
+
 int fpmgpu_host_alloc(int64_t bytes, void** ptr) {
     return guarded([&] { ck(cudaHostAlloc(ptr, size_t(std::max<int64_t>(bytes, 1)), cudaHostAllocPortable), "cudaHostAlloc"); });
 }

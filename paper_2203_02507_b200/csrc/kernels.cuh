@@ -131,6 +131,9 @@ cudaError_t launch_loop64(int mode, bool prune, int meas, int G, const CUtensorM
 cudaError_t launch_lines(int which, int N, const LinesArgs& a, int T, cudaStream_t s);
 // the box-pruned passes for N = 256 (a.box0, a.boxn multiples of 16; which as above)
 cudaError_t launch_lines_box(int which, const LinesArgs& a, int T, cudaStream_t s);
+// batched 2-D complex128 FFT, sides with factors 2, 3, 5 up to 4096 (fft_c128.cu)
+bool fft_c128_supported(int n);
+cudaError_t fft2_c128(double2* data, double2* tmp, long long batch, int rows, int cols, bool inv, cudaStream_t s);
 cudaError_t launch_build_pupils(float2* pupils, const uint8_t* support, const double* defocus,
                                 int n, int T, double dk, double inv_l2, cudaStream_t s);
 

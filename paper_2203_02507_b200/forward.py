@@ -17,9 +17,12 @@ match the double-precision oracle:
 * the grey scale anchored to the on-axis frame (else the brightest,
   forward.cpp:259-268) and quantisation with lround + clamp (forward.cpp:145-160).
 
-All LEDs of a tile run as one batched transform. The transforms are
-torch.fft (cuFFT) in complex128: this is the test-fixture path, not the
-reconstruction hot path (which uses only this repo's kernels). Photon noise,
+All LEDs of a tile run as one batched transform. On the device the 2-D
+transforms are this repo's complex128 Stockham kernel (`fft_c128.cu`, radix
+2/3/4/5: the guard-banded grids are 96 / 120 / 384 / 480 / 512 ... points, not
+the power-of-two sides of the reconstruction kernels); shifts, the transfer
+function, |.|^2 and the feathered assembly are elementwise torch ops. This is
+the fixture path, not the reconstruction hot path. Photon noise,
 when requested, draws from torch's Poisson generator, not the reference's
 std::mt19937_64 stream, so noisy frames are statistically — not bitwise —
 equivalent.
@@ -59,12 +62,36 @@ def _axis_weights(origins, n):
     return w
 
 
+def fft2_c128(x, inverse=False):
+    """2-D FFT over the last two axes of a complex128 CUDA tensor on this repo's
+    kernel (fpmgpu_fft2_c128: Stockham radix 2/3/4/5 in double, any side with
+    factors 2, 3, 5 up to 4096); numpy / torch.fft conventions (the inverse
+    divides by rows * cols)."""
+    import ctypes as C
+
+    import torch
+    from ._lib import check, lib
+    from .engine import default_engine
+    y = x.contiguous().clone()
+    rows, cols = int(y.shape[-2]), int(y.shape[-1])
+    batch = int(y.numel() // max(rows * cols, 1))
+    eng = default_engine(y.device.index if y.device.index is not None else torch.cuda.current_device())
+    check(lib().fpmgpu_fft2_c128(eng.handle, C.c_void_p(y.data_ptr()), batch, rows, cols, 1 if inverse else 0,
+                                 C.c_void_p(torch.cuda.current_stream(y.device).cuda_stream)))
+    return y
+
+
 def _centered(x, inverse=False):
     """fftshift(FFT(ifftshift(x))) over the last two axes (field.cpp:48-87); the
-    inverse divides by rows * cols."""
+    inverse divides by rows * cols. On the device the transform is this repo's
+    FP64 kernel (fft2_c128); the CPU path (device="cpu", the CPU tests) uses
+    torch.fft."""
     import torch
     y = torch.fft.ifftshift(x, dim=(-2, -1))
-    y = torch.fft.ifft2(y) if inverse else torch.fft.fft2(y)
+    if y.is_cuda:
+        y = fft2_c128(y, inverse)
+    else:
+        y = torch.fft.ifft2(y) if inverse else torch.fft.fft2(y)
     return torch.fft.fftshift(y, dim=(-2, -1))
 
 

@@ -194,3 +194,27 @@ def test_acceptance_stitch_continuity_on_device(orc):
     jump_ov = 0.5 * (_seam_phase_jump(with_ov, 243 * up, True) + _seam_phase_jump(with_ov, 243 * up, False))
     jump_no = 0.5 * (_seam_phase_jump(no_ov, 256 * up, True) + _seam_phase_jump(no_ov, 256 * up, False))
     assert jump_ov < 0.2 * jump_no, (jump_ov, jump_no)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(3, 96, 120), (2, 384, 480), (1, 512, 512), (5, 60, 75), (2, 1024, 2048)])
+def test_fft2_c128_matches_numpy(shape):
+    """The forward model's FP64 2-D FFT (fpmgpu_fft2_c128, radix 2/3/4/5) against
+    numpy on the guard-banded tile sizes: forward and inverse to 1e-12 relative."""
+    import torch
+    from paper_2203_02507_b200.forward import fft2_c128
+    rng = np.random.default_rng(sum(shape))
+    x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    t = torch.from_numpy(x).cuda()
+    for inverse, ref in ((False, np.fft.fft2(x)), (True, np.fft.ifft2(x))):
+        got = fft2_c128(t, inverse).cpu().numpy()
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12, (shape, inverse)
+
+
+@pytest.mark.gpu
+def test_fft2_c128_sizes_refused():
+    """Sides with a prime factor above 5 have no kernel: UnsupportedError, not a fallback."""
+    import torch
+    from paper_2203_02507_b200.forward import fft2_c128
+    with pytest.raises(fpm.UnsupportedError, match="factor into 2, 3 and 5"):
+        fft2_c128(torch.zeros((2, 49, 64), dtype=torch.complex128, device="cuda"))
