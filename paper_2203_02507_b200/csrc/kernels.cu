@@ -58,6 +58,9 @@ constexpr int kGroupThreads = 128;
 #ifndef FPM_MOD_SEL
 #define FPM_MOD_SEL 0  // |e| = 0 rule by selects (1; measured +1.5%) or by a 2^-60 nudge of Re (0)
 #endif
+#ifndef FPM_P0_INPUT_SWAP
+#define FPM_P0_INPUT_SWAP 1  // pass 0 step 1: swap the disk's inputs within the pair, not the outputs
+#endif
 #ifndef FPM_O_SMEM
 #define FPM_O_SMEM 0  // EPRY: the gathered canvas values kept in shared memory for the scatter (+8 KB per CTA)
 #endif
@@ -111,13 +114,42 @@ __device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const 
     // step 1: DFT8 over n1r (registers), then the pair DFT over n1c (DIT). Pruned IFFT
     // (skip_cols): only rows a in [2, 6) of columns j in {1, 2} hold data, and the
     // zero entries are never read (they need no initialisation)
+#if FPM_P0_INPUT_SWAP
+    if (skip_cols) {
+        // Columns first, over the disk's four non-zero column digits b in [2, 6) (rows a in
+        // [2, 6)): the pair swaps its two values per row (16 shuffles instead of the 64 of
+        // the output exchange), then each lane forms its four DFT8 outputs k = 4h + m
+        // directly: X = E + (-1)^h O, E from x2, x4 and O from x3, x5
+        //   E = (x2 + x4, -i x2 - x4, x4 - x2, i x2 - x4),
+        //   O = (s, (q - s) / sqrt2, -q, (q + s) / sqrt2), s = x3 + x5, q = -i (x3 - x5).
+        // Exact outputs: pass 0 uses the unscaled column-twiddle table.
+        const float sgr = sg * 0.70710678118654752440f;
+#pragma unroll
+        for (int a = 2; a < 6; ++a) {
+            const float2 o1 = v[a][1], o2 = v[a][2];  // own: x[2 + h], x[4 + h]
+            const float2 r1 = shfl_pair(o1), r2 = shfl_pair(o2);
+            const float2 x2 = h ? r1 : o1, x4 = h ? r2 : o2, x3 = h ? o1 : r1, x5 = h ? o2 : r2;
+            const float2 s24 = cadd(x2, x4), s35 = cadd(x3, x5), q = w8_2<false>(csub(x3, x5));
+            const float2 m2 = w8_2<false>(x2);
+            v[a][0] = cfma(sg, s35, s24);
+            v[a][2] = cfma(-sg, q, csub(x4, x2));
+            v[a][1] = cfma(sgr, csub(q, s35), csub(m2, x4));
+            v[a][3] = cfma(sgr, cadd(q, s35), cneg(cadd(m2, x4)));
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+            dft8<false, true>(v[0][m], v[1][m], v[2][m], v[3][m], v[4][m], v[5][m], v[6][m], v[7][m]);
+    }
+#else
     if (skip_cols) {
 #pragma unroll
         for (int j = 1; j < 3; ++j)
             dft8<false, true>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
 #pragma unroll
         for (int a = 0; a < 8; ++a) dft4_z03<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
-    } else {
+    }
+#endif
+    if (!skip_cols) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             dft8<false, false>(v[0][j], v[1][j], v[2][j], v[3][j], v[4][j], v[5][j], v[6][j], v[7][j]);
@@ -129,6 +161,7 @@ __device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const 
     // rotation (one FFMA2 on the odd lane instead of a complex multiply): the odd lane forms
     // E - s R exactly, the even lane +-(sqrt(2) E + R), whose factor +-s rides on its column
     // twiddle (table entries pre-scaled)
+    if (!(FPM_P0_INPUT_SWAP && skip_cols)) {
 #if FPM_PAIR_ROT
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
@@ -150,6 +183,7 @@ __device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const 
         for (int m = 0; m < 4; ++m) v[a][m] = cfma(sg, v[a][m], shfl_pair(v[a][m]));  // E + O' | E - O'
     }
 #endif
+    }
     // twiddle W64^(n0r k0r + n0c k0c), k0 = (a, 4h + m); table entries (w, (-w.y, w.x))
 #pragma unroll
     for (int a = 1; a < 8; ++a) {
@@ -159,7 +193,8 @@ __device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const 
     }
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        const float4 w = W4_s[64 + m * 16 + 2 * tc + h];  // = W64^(tc (4h + m)), in lane order
+        // = W64^(tc (4h + m)), in lane order; [128, 192): the same without the pair trick's scale
+        const float4 w = W4_s[((FPM_P0_INPUT_SWAP && skip_cols) ? 128 : 64) + m * 16 + 2 * tc + h];
 #pragma unroll
         for (int a = 0; a < 8; ++a) v[a][m] = cmul_sw(v[a][m], make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
@@ -269,7 +304,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
     size_t b = 1024;                                              // alignment slack (128B-swizzled TMA box)
     b += size_t(G) * kGroupBytes;                                 // per-group staging + transpose
     b += size_t(nslots) * kGroupThreads * sizeof(float2);         // lattice pupil [NP][128]
-    b += 128 * sizeof(float4);                                    // W64 table + column-twiddle table
+    b += 192 * sizeof(float4);                                    // W64 table + column-twiddle tables
     b += size_t(iters) * sizeof(double);                          // stage sums
     b += size_t(G) * (sizeof(uint64_t) + 16 * sizeof(float));     // mbarriers + reductions
     b += size_t(L) * (sizeof(short2) + sizeof(int) + sizeof(float) + 1);  // origins, frame map, sum(I), bright flags
@@ -281,7 +316,7 @@ size_t loop_smem_bytes(int G, int nslots, int L, int iters) {
 // MINB: resident tiles per SM the register budget is sized for (4: 128 registers,
 // the throughput build; 2: 255 registers, lower latency per update for batches
 // that leave SMs with at most a few tiles)
-template <int MODE, bool PRUNE, int MEAS, int G, int N, int MINB>
+template <int MODE, bool PRUNE, int MEAS, int G, int N, int MINB, bool JIT>
 __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     fpm_loop64(const __grid_constant__ CUtensorMap tmap, const LoopArgs args) {
     using Lat = Lattice<PRUNE>;
@@ -305,7 +340,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     // [0, 64): (W64^m, swizzled), m in [0, 64); [64, 128): the column twiddle W64^(tc (4h + m))
     // at 64 + 16 m + 2 tc + h, i.e. in lane order (lane = 2 (8 tr + tc) + h): conflict-free
     float4* W4_s = reinterpret_cast<float4*>(smem + off);
-    off += 128 * sizeof(float4);
+    off += 192 * sizeof(float4);
     double* stage_sum = reinterpret_cast<double*>(smem + off);
     off += size_t(args.iters) * sizeof(double);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off);
@@ -329,13 +364,14 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     float* rg = red + g * 16;
 
     // ---- one-time setup: W64 tables, pair twiddles, mbarrier
-    if (threadIdx.x < 128) {
-        const int t = threadIdx.x, e = t - 64;
+    for (int t = threadIdx.x; t < 192; t += blockDim.x) {
+        const int e = (t - 64) & 63;  // column tables: [64, 128) pre-scaled, [128, 192) exact
         const int m = t < 64 ? t : ((((e & 15) >> 1) * (4 * (e & 1) + (e >> 4))) & 63);
         double s, c;
         sincospi(-double(m) / 32.0, &s, &c);
         // column twiddles of the even lane for m = 1, 3 carry the pair combine's +-1/sqrt(2)
-        const double f = (FPM_PAIR_ROT && t >= 64 && (e & 1) == 0 && ((e >> 4) & 1)) ? ((e >> 4) == 1 ? 1.0 : -1.0) * 0.70710678118654752440 : 1.0;
+        const double f = (FPM_PAIR_ROT && t >= 64 && t < 128 && (e & 1) == 0 && ((e >> 4) & 1))
+                             ? ((e >> 4) == 1 ? 1.0 : -1.0) * 0.70710678118654752440 : 1.0;
         W4_s[t] = make_float4(float(c * f), float(s * f), -float(s * f), float(c * f));
     }
     // pair-combine twiddles W8^m, m = 1..3, on the odd lane (1 on the even lane)
@@ -384,7 +420,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                 __threadfence();
                 st_release_gpu(args.work + 1 + jp % args.T, jp / args.T + 1);
             }
-            jitter_sleep(args, -1 - round);
+            jitter_sleep<JIT>(args, -1 - round);
             const int j = atomicAdd(args.work, 1);
             *item_s = j;
             if (j < n_items && j >= args.T) {  // acquire: the tile's previous pass is complete
@@ -445,7 +481,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     // sequential slots (G == 1): (iteration, position) by counters, not a division per slot
     int c_it = G == 1 ? s_begin / L : 0, c_pos = G == 1 ? s_begin - c_it * L : 0;
     for (int s = s_begin; s < s_end; ++s) {
-        jitter_sleep(args, s);
+        jitter_sleep<JIT>(args, s);
         const int2 e = G == 1 ? make_int2(c_it, c_pos) : slot_entry<G>(args, s, g);
         if (e.x >= 0) {
             if (!issued) issue(e);
@@ -700,7 +736,7 @@ static int queue_override() {
 template <int MODE, bool PRUNE, int MEAS, int G, int N, int MINB>
 static cudaError_t launch_loop_t(const CUtensorMap* tmap, const LoopArgs& a0, int T, cudaStream_t s) {
     const size_t smem = loop_smem_bytes(G, a0.nslots, a0.L, a0.iters);
-    auto k = fpm_loop64<MODE, PRUNE, MEAS, G, N, MINB>;
+    auto k = a0.jitter > 0 ? fpm_loop64<MODE, PRUNE, MEAS, G, N, MINB, true> : fpm_loop64<MODE, PRUNE, MEAS, G, N, MINB, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     LoopArgs a = a0;

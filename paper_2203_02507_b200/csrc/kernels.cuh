@@ -103,7 +103,13 @@ cudaError_t launch_loop64q(int mode, const CUtensorMap* tmap, const LoopArgs& a,
 // sleeps a pseudo-random 0..jitter ns before every update and work-queue claim, so a
 // missing barrier, fence or dependency wait shows up as run-to-run bit differences
 // (tests/test_race_jitter.py; compute-sanitizer is closed on the GPU pool).
+// JIT is a template flag of every loop kernel: the production instantiations
+// compile the hook out (the runtime test alone cost 1.2% of the config-3 loop,
+// profiles/r2/jitter_cost.txt); the launchers pick the JIT ones only when
+// FPM_B200_JITTER is set.
+template <bool JIT>
 __device__ __forceinline__ void jitter_sleep(const LoopArgs& a, int step) {
+    if constexpr (!JIT) return;
     if (a.jitter > 0) {
         unsigned h = a.jitter_seed ^ (blockIdx.x * 0x9E3779B1u) ^ (unsigned(step) * 0x85EBCA77u) ^
                      ((threadIdx.x >> 5) * 0xC2B2AE3Du);

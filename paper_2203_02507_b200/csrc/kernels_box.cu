@@ -40,7 +40,7 @@ size_t box_smem_bytes(int n, int box, int L, int iters, bool scratch_in_smem) {
     return b;
 }
 
-template <int NLR, int MODE, int NC, bool SMEM_S>
+template <int NLR, int MODE, int NC, bool SMEM_S, bool JIT>
 __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs args, BoxArgs bx) {
     constexpr int M = NLR / 32;
     constexpr int RS = NLR + 1;
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
     // the whole CTA — they touch disjoint disks, so any order equals the concurrent one
     const int G = args.slots ? 2 : 1;
     for (int e = args.slot_begin * G; e < args.num_slots * G; ++e) {
-        jitter_sleep(args, e);
+        jitter_sleep<JIT>(args, e);
         int it, pos;
         if (G == 1) {
             it = e / L;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
 template <int NLR, int MODE, int NC, bool SMEM_S>
 static cudaError_t launch_box_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s) {
     const size_t smem = box_smem_bytes(NLR, b.box, a.L, a.iters, SMEM_S);
-    auto k = fpm_loop_box<NLR, MODE, NC, SMEM_S>;
+    auto k = a.jitter > 0 ? fpm_loop_box<NLR, MODE, NC, SMEM_S, true> : fpm_loop_box<NLR, MODE, NC, SMEM_S, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     k<<<T, kBoxThreads, smem, s>>>(a, b);

@@ -125,7 +125,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int NLR, int MODE, int NC, int CL, int NW>
+template <int NLR, int MODE, int NC, int CL, int NW, bool JIT>
 __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32)) fpm_loop_cluster(const LoopArgs args, const BoxArgs bx) {
     constexpr int M = NLR / 32;
     constexpr int SW = NLR / CL;  // columns per CTA
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(args.work + 1 + jp % args.T), "r"(jp / args.T + 1)
                              : "memory");
             }
-            jitter_sleep(args, -1 - round);
+            jitter_sleep<JIT>(args, -1 - round);
             const int j = atomicAdd(args.work, 1);
             if (j < n_items && j >= args.T) {  // acquire: the tile's previous pass is complete
                 const int* flag = args.work + 1 + (j % args.T);
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         stage(pos0);
     }
     for (; e >= 0;) {
-        jitter_sleep(args, e);
+        jitter_sleep<JIT>(args, e);
         int it, pos;
         entry_at(e, it, pos);
         float2* const S = par ? S1 : S0;
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
 template <int NLR, int MODE, int NC, int CL, int NW>
 cudaError_t launch_cluster_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s) {
     const size_t smem = cluster_smem_bytes(NLR, b.box, CL, NW, a.L, a.iters);
-    auto k = fpm_loop_cluster<NLR, MODE, NC, CL, NW>;
+    auto k = a.jitter > 0 ? fpm_loop_cluster<NLR, MODE, NC, CL, NW, true> : fpm_loop_cluster<NLR, MODE, NC, CL, NW, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     if (CL > 8) {  // 16-CTA clusters are a non-portable size on sm_100

@@ -201,7 +201,7 @@ size_t loop64q_smem_bytes(int L, int iters, bool osep) {
     return b;
 }
 
-template <int MODE, int N, int MINB>
+template <int MODE, int N, int MINB, bool JIT>
 __global__ void __launch_bounds__(kQThreads, MINB)
     fpm_loop64q(const __grid_constant__ CUtensorMap tmap, const LoopArgs args) {
     extern __shared__ uint8_t smem_raw[];
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
                 __threadfence();
                 st_release_gpu(args.work + 1 + jp % args.T, jp / args.T + 1);
             }
-            jitter_sleep(args, -1 - round);
+            jitter_sleep<JIT>(args, -1 - round);
             const int j = atomicAdd(args.work, 1);
             *item_s = j;
             if (j < n_items && j >= args.T) {
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
     };
     int c_it = s_begin / L, c_pos = s_begin - c_it * L;
     for (int s = s_begin; s < s_end; ++s) {
-        jitter_sleep(args, s);
+        jitter_sleep<JIT>(args, s);
         if (!issued) issue(c_pos);
         issued = false;
         const short2 o = O_s[c_pos];
@@ -512,7 +512,7 @@ static int queue_override_q() {
 template <int MODE, int N, int MINB>
 static cudaError_t launch_q_t(const CUtensorMap* tmap, const LoopArgs& a0, int T, cudaStream_t s) {
     const size_t smem = loop64q_smem_bytes(a0.L, a0.iters, MINB == 2);
-    auto k = fpm_loop64q<MODE, N, MINB>;
+    auto k = a0.jitter > 0 ? fpm_loop64q<MODE, N, MINB, true> : fpm_loop64q<MODE, N, MINB, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     LoopArgs a = a0;
