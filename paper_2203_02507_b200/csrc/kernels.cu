@@ -53,7 +53,7 @@ constexpr int kGroupThreads = 128;
 #define FPM_O_STAGE 0
 #endif
 #ifndef FPM_O_EARLY
-#define FPM_O_EARLY 0  // 1: the scatter's old canvas values loaded before pass 1's step 2 (measured 31.24 vs 31.16 ms)
+#define FPM_O_EARLY 1  // 1: the scatter's old canvas values loaded before pass 1's step 2 (loop 30.455 vs 30.57 ms; before the alternating transposes 31.24 vs 31.16)
 #endif
 #ifndef FPM_MOD_SEL
 #define FPM_MOD_SEL 0  // |e| = 0 rule by selects (1; measured +1.5%) or by a 2^-60 nudge of Re (0)
@@ -632,7 +632,9 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                 } else {
                     dsum = D_s[e.y];
                 }
-                stage_sum[e.x] += dsum > 0.f ? double(nsum) / double(dsum) : 0.0;
+                // the update's ratio in FP32 (an FP64 division here cost 0.6% of the loop,
+                // profiles/r2/variants_r2.txt), the pass sum in FP64
+                stage_sum[e.x] += dsum > 0.f ? double(__fdividef(nsum, dsum)) : 0.0;
             }
             if (MODE == kModeEPRY) {
                 const float om = fmaxf(fmaxf(rg[8], rg[9]), fmaxf(rg[10], rg[11]));

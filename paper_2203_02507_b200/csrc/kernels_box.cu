@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
                 nsum += red[k * 4];
                 dsum += red[k * 4 + 1];
             }
-            stage_sum[it] += dsum > 0.f ? double(nsum) / double(dsum) : 0.0;
+            stage_sum[it] += dsum > 0.f ? double(__fdividef(nsum, dsum)) : 0.0;  // as fpm_loop64
         }
         float inv_omax = 0.f, inv_pmax = 0.f;
         if (MODE == kModeEPRY) {

@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 a3 = fmaxf(a3, __shfl_xor_sync(kFull, a3, sh));
             }
             if (l == 0) {
-                if (rank == 0) stage_sum[it] += a1 > 0.f ? double(a0) / double(a1) : 0.0;
+                if (rank == 0) stage_sum[it] += a1 > 0.f ? double(__fdividef(a0, a1)) : 0.0;  // as fpm_loop64
                 upd[0] = (a2 > 0.f && B_s[pos]) ? args.beta / a2 : 0.f;  // bright-field pupil steps only
                 upd[1] = a3 > 0.f ? args.alpha / a3 : 0.f;
             }

@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
             } else {
                 dsum = D_s[c_pos];
             }
-            stage_sum[c_it] += dsum > 0.f ? double(nsum) / double(dsum) : 0.0;
+            stage_sum[c_it] += dsum > 0.f ? double(__fdividef(nsum, dsum)) : 0.0;  // as fpm_loop64
         }
         float inv_omax = 0.f, inv_pmax = 0.f;
         if (MODE == kModeEPRY) {
