@@ -366,6 +366,7 @@ void build_plan(fpmgpu_plan& p, const fpmgpu_recon_request& r) {
         p.sup_rows.upload(runs.data(), runs.size(), p.ctx->stream);
         if (fpmk::cluster_smem_bytes(p.n, p.box, p.cl, fpmk::cluster_warps(p.n, p.cl), p.L, r.iters) > 232448)
             throw Unsupported("cluster slab exceeds shared memory");
+        if (p.F > 65536) throw Unsupported("the cluster kernel indexes at most 65,536 frames");
     } else if (p.use_box) {
         box_of(sup, p.n, &p.b0, &p.box);
         const bool smem_s = p.n != 256;

@@ -1,11 +1,20 @@
 // Kernel launch interface shared by capi.cu and kernels.cu.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace fpmk {
+
+// FPM_B200_MID=0: the n = 256 box / cluster kernels without the [64, 192) box
+// pruning of WarpFFT256 (tests compare the two)
+inline bool mid_disabled() {
+    const char* e = std::getenv("FPM_B200_MID");
+    return e && e[0] == '0';
+}
 
 enum { kModeGS = 0, kModeEPRY = 1 };
 

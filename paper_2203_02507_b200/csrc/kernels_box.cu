@@ -37,10 +37,12 @@ size_t box_smem_bytes(int n, int box, int L, int iters, bool scratch_in_smem) {
     b += size_t(iters) * sizeof(double) + 16;
     b += size_t(kBoxWarps) * 4 * sizeof(float);
     b += size_t(L) * (sizeof(short2) + sizeof(int) + 1) + 16;
+    b = (b + 15) & ~size_t(15);
+    if (n == 256) b += size_t(kBoxWarps) * WarpFFT256<false>::kBufFloat2 * sizeof(float2);  // FFT transposes
     return b;
 }
 
-template <int NLR, int MODE, int NC, bool SMEM_S, bool JIT>
+template <int NLR, int MODE, int NC, bool SMEM_S, bool JIT, bool MID>
 __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs args, BoxArgs bx) {
     constexpr int M = NLR / 32;
     constexpr int RS = NLR + 1;
@@ -67,6 +69,10 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
     int* F_s = reinterpret_cast<int*>(sp);
     sp += size_t(L) * sizeof(int);
     uint8_t* B_s = sp;
+    sp += size_t(L);
+    sp = smem_raw + ((sp - smem_raw + 15) & ~15);
+    using FFT = typename WarpFFTSel<M, MID>::type;
+    float2* TB = reinterpret_cast<float2*>(sp) + size_t(w) * FFT::kBufFloat2;  // n = 256: this warp's transpose buffer
 
     float2* canvas = args.canvas + size_t(tile) * NC * NC;
     float2* pupil = args.pupils + size_t(tile) * NLR * NLR;
@@ -78,8 +84,8 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
         B_s[k] = MODE == kModeEPRY ? args.bright[size_t(tile) * L + k] : 0;
     }
     for (int k = threadIdx.x; k < args.iters; k += blockDim.x) stage_sum[k] = 0.0;
-    WarpFFT<M> F;
-    F.init(l, NLR);
+    FFT F;
+    F.init(l, NLR, TB);
     const float inv_n2 = 1.0f / float(NLR * NLR);
     __syncthreads();
 
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
             const uint16_t* fr = bx.frames + size_t(F_s[pos]) * bx.frame_stride + size_t(txy.y) * bx.pitch + txy.x;
             for (int idx = threadIdx.x; idx < NLR * NLR; idx += kBoxThreads) {
                 const int r = idx / NLR, c = idx % NLR;
-                I_s[r * NLR + (c ^ (2 * (r / M)))] = fr[size_t(r) * bx.pitch + c];
+                I_s[r * NLR + (c ^ FFT::isw(r))] = fr[size_t(r) * bx.pitch + c];
             }
         }
 
@@ -118,9 +124,9 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
             float2 x[M];
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
-                const int c = k0 + M * brev5(l);
+                const int c = F.a_in(k0);
                 float2 v = make_float2(0.f, 0.f);
-                if (sup[i * NLR + c]) {
+                if (FFT::live(k0) && sup[i * NLR + c]) {
                     const float2 O = cvc[size_t(i) * NC + c];
                     const float2 P = pupil[i * NLR + c];
                     const float2 g = cmul(O, P);  // conj, signed: the row IFFT runs as conj(FFT(conj g))
@@ -132,9 +138,9 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
                 }
                 x[k0] = v;
             }
-            F.f2(x);  // S keeps conj(IFFT_rows(g)): phase B's forward column FFT undoes it
+            F.fA(x);  // S keeps conj(IFFT_rows(g)): phase B's forward column FFT undoes it
 #pragma unroll
-            for (int r = 0; r < M; ++r) S[size_t(i - b0) * RS + l + 32 * r] = x[r];
+            for (int r = 0; r < M; ++r) S[size_t(i - b0) * RS + F.a_out(r)] = x[r];
         }
         if (MODE == kModeEPRY) {
 #pragma unroll
@@ -155,37 +161,38 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
             float2 x[M];
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                const int r = l + 32 * m;
-                x[m] = (r >= b0 && r < b0 + B) ? S[size_t(r - b0) * RS + j] : make_float2(0.f, 0.f);
+                const int r = F.nat(m);
+                x[m] = (FFT::live(m) && r >= b0 && r < b0 + B) ? S[size_t(r - b0) * RS + j] : make_float2(0.f, 0.f);
             }
             F.f1(x);  // = conj(e), e the unscaled 2-D IFFT
+            const uint16_t* Ic = I_s + (j ^ F.isw_lane());  // one column swizzle per lane
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
-                const int row = k0 + M * brev5(l);
+                const int row = F.scr(k0);
                 float Iv;
                 if (args.meas_f32 == nullptr) {
-                    Iv = float(I_s[row * NLR + (j ^ (2 * (row / M)))]);
+                    Iv = float(Ic[row * NLR]);
                 } else {
                     Iv = args.meas_f32[row * NLR + j];
                 }
                 den += Iv;
-                // branch-free: |e|^2 at or below FLT_MIN counts as |e| = 0 (recon.cpp:122)
+                // |e| = 0 rule (recon.cpp:122) as in fpm_loop64: Re nudged by sgn 2^-60 maps
+                // e = 0 to e' = sgn sqrt(I) (checkerboard sign), leaves |Re| >= 2^-35 exact
                 const float meas = sqrt_ftz(Iv);
                 const float2 u = x[k0];
-                const float m2 = cabs2(u);
-                const bool nz = m2 > kTiny;
+                const float ux = u.x + (((row + j) & 1) ? -0x1p-60f : 0x1p-60f);
+                const float m2 = fmaf(ux, ux, u.y * u.y);
                 const float rr = rsqrt_ftz(fmaxf(m2, kTiny));
                 const float dm = fmaf(m2 * rr, inv_n2, -meas);
                 num = fmaf(dm, dm, num);
-                const float sc = nz ? meas * rr : 0.f;
-                const float z = nz ? 0.f : (((row + j) & 1) ? -meas : meas);
-                x[k0] = make_float2(fmaf(u.x, sc, z), -u.y * sc);  // e' from u = conj(e)
+                const float sc = meas * rr;
+                x[k0] = make_float2(ux * sc, -u.y * sc);  // e' from u = conj(e)
             }
             F.f2(x);
 #pragma unroll
             for (int r = 0; r < M; ++r) {
-                const int row = l + 32 * r;
-                if (row >= b0 && row < b0 + B) S[size_t(row - b0) * RS + j] = x[r];
+                const int row = F.nat(r);
+                if (FFT::live(r) && row >= b0 && row < b0 + B) S[size_t(row - b0) * RS + j] = x[r];
             }
         }
 #pragma unroll
@@ -221,12 +228,12 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
         for (int i = b0 + w; i < b0 + B; i += kBoxWarps) {
             float2 x[M];
 #pragma unroll
-            for (int m = 0; m < M; ++m) x[m] = S[size_t(i - b0) * RS + l + 32 * m];
-            F.f1(x);
+            for (int m = 0; m < M; ++m) x[m] = S[size_t(i - b0) * RS + F.c_in(m)];
+            F.fC(x);
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
-                const int c = k0 + M * brev5(l);
-                if (!sup[i * NLR + c]) continue;
+                const int c = F.c_out(k0);
+                if (!FFT::live(k0) || !sup[i * NLR + c]) continue;
                 const float2 psi2 = cscale(x[k0], ((i + c) & 1) ? -1.f : 1.f);
                 float2* dst = cv + size_t(i) * NC + c;
                 float2* pp = pupil + i * NLR + c;
@@ -249,7 +256,11 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
 template <int NLR, int MODE, int NC, bool SMEM_S>
 static cudaError_t launch_box_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s) {
     const size_t smem = box_smem_bytes(NLR, b.box, a.L, a.iters, SMEM_S);
-    auto k = a.jitter > 0 ? fpm_loop_box<NLR, MODE, NC, SMEM_S, true> : fpm_loop_box<NLR, MODE, NC, SMEM_S, false>;
+    auto k = a.jitter > 0 ? fpm_loop_box<NLR, MODE, NC, SMEM_S, true, false> : fpm_loop_box<NLR, MODE, NC, SMEM_S, false, false>;
+    if constexpr (NLR == 256) {  // the support box inside [64, 192): WarpFFT256 pruned to registers 2..5
+        if (b.b0 >= 64 && b.b0 + b.box <= 192 && !mid_disabled())
+            k = a.jitter > 0 ? fpm_loop_box<NLR, MODE, NC, SMEM_S, true, true> : fpm_loop_box<NLR, MODE, NC, SMEM_S, false, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     k<<<T, kBoxThreads, smem, s>>>(a, b);

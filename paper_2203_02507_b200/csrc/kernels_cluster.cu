@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "warp_fft.cuh"
@@ -37,7 +38,7 @@ namespace cg = cooperative_groups;
 #define FPM_CL_DB256 0  // n = 256 on 8-CTA clusters: double-buffered slabs (st.async + mbarrier, no end-of-update barrier)
 #endif
 #ifndef FPM_CL_PF8
-#define FPM_CL_PF8 0  // 1: row prefetch for n = 256 too (more registers per thread)
+#define FPM_CL_PF8 1  // n = 256: the next row's disk loads in flight in registers (phase A; with the MID pruning only 4 registers: 484 vs 516 ms)
 #endif
 
 namespace fpmk {
@@ -46,13 +47,16 @@ namespace fpmk {
 #define FPM_CL_STAGE_C 1  // n = 256: phase-C scatter operands staged the same way, under the row's FFT
 #endif
 #ifndef FPM_CL_STAGE
-#define FPM_CL_STAGE 1  // n = 256: phase-A canvas/pupil box rows staged one row ahead by cp.async (per warp)
+#define FPM_CL_STAGE 0  // 1: n = 256 on the shuffle FFT with canvas/pupil box rows staged one row ahead by cp.async
 #endif
 
-// n = 256 row staging: per warp one box row of canvas and pupil, box columns
-// rounded up to 16 (the XOR swizzle below stays inside each group of 16)
+// n = 256: per warp the 16 x 17 transpose buffer of WarpFFT256 (FPM_CL_STAGE=1, the
+// round-2 shuffle FFT: one box row of canvas and pupil staged per warp instead, box
+// columns rounded up to 16 so the XOR swizzle below stays inside each group of 16)
 __host__ __device__ static size_t row_stage_bytes(int n, int box, int nw) {
-    return (FPM_CL_STAGE && n == 256) ? size_t(nw) * 2 * size_t((box + 15) & ~15) * sizeof(float2) : 0;
+    if (n != 256) return 0;
+    return FPM_CL_STAGE ? size_t(nw) * 2 * size_t((box + 15) & ~15) * sizeof(float2)
+                        : size_t(nw) * WarpFFT256<false>::kBufFloat2 * sizeof(float2);
 }
 
 size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
@@ -65,7 +69,7 @@ size_t cluster_smem_bytes(int n, int box, int cl, int nw, int L, int iters) {
     b += row_stage_bytes(n, box, nw);                     // phase-A row staging (n = 256)
     b += size_t(iters) * sizeof(double) + 2 * sizeof(uint64_t);
     b += nbuf * size_t(nw) * 4 * sizeof(float) + 4 * sizeof(float);
-    b += size_t(L) * (sizeof(short2) + sizeof(int) + 1) + 16;
+    b += size_t(L) * (sizeof(short2) + sizeof(uint16_t) + 1) + 16;
     b += 8;  // work-queue item
     return b;
 }
@@ -125,17 +129,17 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int NLR, int MODE, int NC, int CL, int NW, bool JIT>
+template <int NLR, int MODE, int NC, int CL, int NW, bool JIT, bool MID>
 __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32)) fpm_loop_cluster(const LoopArgs args, const BoxArgs bx) {
     constexpr int M = NLR / 32;
     constexpr int SW = NLR / CL;  // columns per CTA
     constexpr int RS = SW + 1;    // slab row stride (float2): column reads conflict-free
     constexpr int NT = NW * 32;
-    constexpr bool PF = M <= 4 || FPM_CL_PF8;  // register room to keep the next row's disk loads in flight
+    constexpr bool PF = M <= 4 || (FPM_CL_PF8 && !(FPM_CL_STAGE && NLR == 256));  // next row's disk loads in flight
 #ifndef FPM_CL_PFC8
-#define FPM_CL_PFC8 0
+#define FPM_CL_PFC8 1
 #endif
-    constexpr bool PFC = M <= 4 || FPM_CL_PFC8;  // phase C: scatter operands loaded before the FFT
+    constexpr bool PFC = M <= 4 || (FPM_CL_PFC8 && !(FPM_CL_STAGE && NLR == 256));  // phase C: scatter operands loaded before the FFT
     // DB: two slab / reduction buffers used alternately, so an update's phase A never
     // overwrites what the previous update's phase C still reads: no end-of-update barrier
     constexpr bool DB = NLR <= 128 || (FPM_CL_DB256 && NLR == 256 && CL >= 8);
@@ -158,8 +162,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
     sp += size_t(NLR) * sizeof(short2);
     sp = smem_raw + ((sp - smem_raw + 15) & ~15);
     constexpr bool STG = FPM_CL_STAGE && NLR == 256;
+    using FFT = std::conditional_t<STG, WarpFFT<M>, typename WarpFFTSel<M, MID>::type>;
     const int RBW = (B + 15) & ~15;  // staged row width (box columns, XOR-swizzled in groups of 16)
-    float2* RB = reinterpret_cast<float2*>(sp) + size_t(w) * 2 * RBW;  // this warp's [canvas | pupil] row
+    float2* RB = reinterpret_cast<float2*>(sp) + size_t(w) * 2 * RBW;  // STG: this warp's [canvas | pupil] row
+    float2* TB = reinterpret_cast<float2*>(sp) + size_t(w) * FFT::kBufFloat2;  // else: its FFT transpose buffer
     sp += row_stage_bytes(NLR, B, NW);
     double* stage_sum = reinterpret_cast<double*>(sp);
     sp += size_t(args.iters) * sizeof(double);
@@ -176,17 +182,17 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
     sp += 4 * sizeof(float);
     short2* O_s = reinterpret_cast<short2*>(sp);
     sp += size_t(L) * sizeof(short2);
-    int* F_s = reinterpret_cast<int*>(sp);
-    sp += size_t(L) * sizeof(int);
+    uint16_t* F_s = reinterpret_cast<uint16_t*>(sp);  // frame of each position (< 65536, capi.cu)
+    sp += size_t(L) * sizeof(uint16_t);
     uint8_t* B_s = sp;
     sp += size_t(L);
     sp = smem_raw + ((sp - smem_raw + 3) & ~3);
     int* item_s = reinterpret_cast<int*>(sp);  // work queue: the cluster's current item (rank 0's copy)
 
     for (int k = threadIdx.x; k < NLR; k += NT) SR[k] = bx.sup_rows[k];
-    for (int k = threadIdx.x; k < L; k += NT) F_s[k] = args.seq_frame[k];
-    WarpFFT<M> F;
-    F.init(l, NLR);
+    for (int k = threadIdx.x; k < L; k += NT) F_s[k] = uint16_t(args.seq_frame[k]);
+    FFT F;
+    F.init(l, NLR, TB);
     const float inv_n2 = 1.0f / float(NLR * NLR);
     if (DB && threadIdx.x == 0) {
         mbar_init1(mbA);
@@ -278,13 +284,13 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         if (even_x) {
             for (int idx = threadIdx.x; idx < NLR * SW / 2; idx += NT) {
                 const int r = idx / (SW / 2), jp = 2 * (idx % (SW / 2));
-                cp_async4(I_s + r * SW + (jp ^ ((2 * (r / M)) & (SW - 1))), fr + size_t(r) * bx.pitch + jp);
+                cp_async4(I_s + r * SW + (jp ^ (FFT::isw(r) & (SW - 1))), fr + size_t(r) * bx.pitch + jp);
             }
             cp_async_commit();
         } else {
             for (int idx = threadIdx.x; idx < NLR * SW; idx += NT) {
                 const int r = idx / SW, jj = idx % SW;
-                I_s[r * SW + (jj ^ ((2 * (r / M)) & (SW - 1)))] = fr[size_t(r) * bx.pitch + jj];
+                I_s[r * SW + (jj ^ (FFT::isw(r) & (SW - 1)))] = fr[size_t(r) * bx.pitch + jj];
             }
         }
     };
@@ -319,8 +325,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             const short2 run = SR[ii];
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
-                const int c = k0 + M * brev5(l);
-                const bool on = c >= run.x && c < run.y;
+                const int c = F.a_in(k0);
+                const bool on = FFT::live(k0) && c >= run.x && c < run.y;
                 Oa[k0] = on ? cv[size_t(ii) * NC + c] : make_float2(0.f, 0.f);
                 Pa[k0] = on ? pupil[ii * NLR + c] : make_float2(0.f, 0.f);
             }
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             if constexpr (PF) {
 #pragma unroll
                 for (int k0 = 0; k0 < M; ++k0) {
-                    const int c = k0 + M * brev5(l);
+                    const int c = F.a_in(k0);
                     const float2 g = cmul(Oa[k0], Pa[k0]);  // conj, signed: the row IFFT runs as conj(FFT(conj g))
                     x[k0] = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
                     if (MODE == kModeEPRY) {
@@ -360,9 +366,9 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 const short2 run = SR[i];
 #pragma unroll
                 for (int k0 = 0; k0 < M; ++k0) {
-                    const int c = k0 + M * brev5(l);
+                    const int c = F.a_in(k0);
                     float2 v = make_float2(0.f, 0.f);
-                    if (c >= run.x && c < run.y) {
+                    if (FFT::live(k0) && c >= run.x && c < run.y) {
                         const float2 O = RB[rb_slot(c - b0)];
                         const float2 P = RB[RBW + rb_slot(c - b0)];
                         const float2 g = cmul(O, P);
@@ -380,9 +386,9 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 const short2 run = SR[i];
 #pragma unroll
                 for (int k0 = 0; k0 < M; ++k0) {
-                    const int c = k0 + M * brev5(l);
+                    const int c = F.a_in(k0);
                     float2 v = make_float2(0.f, 0.f);
-                    if (c >= run.x && c < run.y) {
+                    if (FFT::live(k0) && c >= run.x && c < run.y) {
                         const float2 O = cv[size_t(i) * NC + c];
                         const float2 P = pupil[i * NLR + c];
                         const float2 g = cmul(O, P);
@@ -395,10 +401,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                     x[k0] = v;
                 }
             }
-            F.f2(x);  // S keeps conj(IFFT_rows(g)): phase B's forward column FFT undoes it
+            F.fA(x);  // S keeps conj(IFFT_rows(g)): phase B's forward column FFT undoes it
 #pragma unroll
             for (int r = 0; r < M; ++r) {
-                const int col = l + 32 * r, owner = col / SW;
+                const int col = F.a_out(r), owner = col / SW;
                 if constexpr (DB) {
                     const uint32_t off = uint32_t((size_t(i - b0) * RS + (col - owner * SW)) * sizeof(float2));
                     st_async_f2(map_rank(smem_addr(S) + off, owner), x[r], map_rank(smem_addr(mbA + par), owner));
@@ -433,32 +439,34 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             float2 x[M];
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                const int r = l + 32 * m;
-                x[m] = (r >= b0 && r < b0 + B) ? S[size_t(r - b0) * RS + jj] : make_float2(0.f, 0.f);
+                const int r = F.nat(m);
+                x[m] = (FFT::live(m) && r >= b0 && r < b0 + B) ? S[size_t(r - b0) * RS + jj] : make_float2(0.f, 0.f);
             }
             F.f1(x);  // = conj(e), e the unscaled 2-D IFFT
+            // every row this lane holds shares one column swizzle (FFT::isw_lane)
+            const uint16_t* Ic = I_s + (jj ^ (F.isw_lane() & (SW - 1)));
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
-                const int row = k0 + M * brev5(l);
-                const float Iv = float(I_s[row * SW + (jj ^ ((2 * brev5(l)) & (SW - 1)))]);
+                const int row = F.scr(k0);
+                const float Iv = float(Ic[row * SW]);
                 den += Iv;
-                // branch-free: |e|^2 at or below FLT_MIN counts as |e| = 0 (recon.cpp:122)
+                // |e| = 0 rule (recon.cpp:122) as in fpm_loop64: Re nudged by sgn 2^-60 maps
+                // e = 0 to e' = sgn sqrt(I) (checkerboard sign), leaves |Re| >= 2^-35 exact
                 const float meas = sqrt_ftz(Iv);
                 const float2 u = x[k0];
-                const float m2 = cabs2(u);
-                const bool nz = m2 > kTiny;
+                const float ux = u.x + (((row + j) & 1) ? -0x1p-60f : 0x1p-60f);
+                const float m2 = fmaf(ux, ux, u.y * u.y);
                 const float rr = rsqrt_ftz(fmaxf(m2, kTiny));
                 const float dm = fmaf(m2 * rr, inv_n2, -meas);
                 num = fmaf(dm, dm, num);
-                const float sc = nz ? meas * rr : 0.f;
-                const float z = nz ? 0.f : (((row + j) & 1) ? -meas : meas);
-                x[k0] = make_float2(fmaf(u.x, sc, z), -u.y * sc);  // e' from u = conj(e)
+                const float sc = meas * rr;
+                x[k0] = make_float2(ux * sc, -u.y * sc);  // e' from u = conj(e)
             }
             F.f2(x);
 #pragma unroll
             for (int r = 0; r < M; ++r) {
-                const int row = l + 32 * r;
-                if (row >= b0 && row < b0 + B) S[size_t(row - b0) * RS + jj] = x[r];
+                const int row = F.nat(r);
+                if (FFT::live(r) && row >= b0 && row < b0 + B) S[size_t(row - b0) * RS + jj] = x[r];
             }
         }
 #pragma unroll
@@ -513,8 +521,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             if constexpr (PFC) {
 #pragma unroll
                 for (int k0 = 0; k0 < M; ++k0) {
-                    const int c = k0 + M * brev5(l);
-                    const bool on = c >= run.x && c < run.y;
+                    const int c = F.c_out(k0);
+                    const bool on = FFT::live(k0) && c >= run.x && c < run.y;
                     Pc[k0] = on ? pupil[i * NLR + c] : make_float2(0.f, 0.f);
                     Oc[k0] = (MODE == kModeEPRY && on) ? cv[size_t(i) * NC + c] : make_float2(0.f, 0.f);
                 }
@@ -523,18 +531,18 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             float2 x[M];
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                const int col = l + 32 * m, owner = col / SW;
+                const int col = F.c_in(m), owner = col / SW;
                 x[m] = cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)];
             }
-            F.f1(x);
+            F.fC(x);
             if constexpr (STG && FPM_CL_STAGE_C) {
                 cp_async_wait_all();
                 __syncwarp();
             }
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
-                const int c = k0 + M * brev5(l);
-                if (c < run.x || c >= run.y) continue;
+                const int c = F.c_out(k0);
+                if (!FFT::live(k0) || c < run.x || c >= run.y) continue;
                 const float2 psi2 = cscale(x[k0], ((i + c) & 1) ? -1.f : 1.f);
                 float2* dst = cv + size_t(i) * NC + c;
                 float2* pp = pupil + i * NLR + c;
@@ -584,7 +592,14 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
 template <int NLR, int MODE, int NC, int CL, int NW>
 cudaError_t launch_cluster_t(const LoopArgs& a, const BoxArgs& b, int T, cudaStream_t s) {
     const size_t smem = cluster_smem_bytes(NLR, b.box, CL, NW, a.L, a.iters);
-    auto k = a.jitter > 0 ? fpm_loop_cluster<NLR, MODE, NC, CL, NW, true> : fpm_loop_cluster<NLR, MODE, NC, CL, NW, false>;
+    // MID (n = 256): the support box inside [64, 192) lets WarpFFT256 prune to registers 2..5
+    auto k = a.jitter > 0 ? fpm_loop_cluster<NLR, MODE, NC, CL, NW, true, false>
+                          : fpm_loop_cluster<NLR, MODE, NC, CL, NW, false, false>;
+    if constexpr (NLR == 256 && !FPM_CL_STAGE) {
+        if (b.b0 >= 64 && b.b0 + b.box <= 192 && !mid_disabled())
+            k = a.jitter > 0 ? fpm_loop_cluster<NLR, MODE, NC, CL, NW, true, true>
+                             : fpm_loop_cluster<NLR, MODE, NC, CL, NW, false, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     if (CL > 8) {  // 16-CTA clusters are a non-portable size on sm_100

@@ -441,6 +441,26 @@ def test_cluster_kernel_matches_box_kernel(eng, monkeypatch, n, cl, mode):
     assert np.allclose(a.metrics.pass_mean_residual, b.metrics.pass_mean_residual, rtol=1e-5)
 
 
+@pytest.mark.parametrize("cl,mode", [("1", "epry"), ("4", "epry"), ("4", "gs")])
+def test_n256_box_pruning_matches_full_transforms(eng, monkeypatch, cl, mode):
+    """WarpFFT256 with the support box inside [64, 192) skips the natural-layout
+    registers 0, 1, 6, 7 (pruned first / last DFT8, no loads or stores for them);
+    FPM_B200_MID=0 runs the full transforms. The two agree to FP32 rounding of
+    signed zeros (bit for bit in practice)."""
+    cfg = fpm.OpticalConfig(tile_size=256, tile_overlap=0, upsample=4, led_scan_rows=5, led_scan_cols=5)
+    fs, _, seq, _ = dataset(cfg, seed=43, defocus_um=6.0)
+    t = fpm.partition_tiles(256, 256, cfg)[0]
+    t.defocus_um = 3.0
+    monkeypatch.setenv("FPM_B200_CLUSTER", cl)
+    monkeypatch.setenv("FPM_B200_MID", "0")
+    a = fpm.reconstruct_tile(fs, t, cfg, 2, seq, mode=mode, engine=fpm.Engine(0))
+    monkeypatch.delenv("FPM_B200_MID")
+    b = fpm.reconstruct_tile(fs, t, cfg, 2, seq, mode=mode, engine=fpm.Engine(0))
+    scale = np.abs(a.hr).max()
+    assert np.abs(a.hr - b.hr).max() <= 1e-6 * scale
+    assert np.allclose(a.metrics.pass_mean_residual, b.metrics.pass_mean_residual, rtol=1e-6)
+
+
 @pytest.mark.parametrize("cl", [4, 8])
 def test_cluster_kernel_n64_matches_oracle(orc, eng, monkeypatch, cl):
     """n = 64 on the cluster kernel (single-tile latency path) against the oracle."""
