@@ -282,10 +282,12 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         const uint16_t* fr =
             bx.frames + size_t(F_s[pos]) * bx.frame_stride + size_t(txy.y) * bx.pitch + txy.x + rank * SW;
         if (even_x) {
-            for (int idx = threadIdx.x; idx < NLR * SW / 2; idx += NT) {
-                const int r = idx / (SW / 2), jp = 2 * (idx % (SW / 2));
-                cp_async4(I_s + r * SW + (jp ^ (FFT::isw(r) & (SW - 1))), fr + size_t(r) * bx.pitch + jp);
-            }
+            // thread t: column pair t mod SW/2 of rows t / (SW/2) + k NT / (SW/2) (no division per copy)
+            static_assert(NT % (SW / 2) == 0, "stage: whole rows per pass");
+            const int jp = 2 * (int(threadIdx.x) % (SW / 2));
+            const uint16_t* src = fr + jp;
+            for (int r = int(threadIdx.x) / (SW / 2); r < NLR; r += NT / (SW / 2))
+                cp_async4(I_s + r * SW + (jp ^ (FFT::isw(r) & (SW - 1))), src + size_t(r) * bx.pitch);
             cp_async_commit();
         } else {
             for (int idx = threadIdx.x; idx < NLR * SW; idx += NT) {
