@@ -182,7 +182,10 @@ def cpu_sample(W: Workload, workers: int):
     from oracle import oracle as orc
     oc = oracle_cfg(W)
     seq = orc.led_sequence("spiral", oc)
-    rows = max(1, min(W.fov // W.n, workers // 4))  # a few seconds of work on every host thread
+    # a few seconds of work on every host thread, and at most ~15 s in all: the tile rows
+    # are capped by a budget of 600 k n = 64-equivalent updates (work ~ n^2 per update)
+    per_row = (W.fov // W.n) * W.leds * W.iters * (W.n / 64) ** 2
+    rows = max(1, min(W.fov // W.n, workers // 4, int(600_000 // per_row)))
     H = W.n * rows
     rng = np.random.default_rng(1)
     imgs = rng.integers(0, 52429, (len(seq), H, W.fov), dtype=np.uint16)
