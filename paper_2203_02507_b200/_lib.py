@@ -10,7 +10,10 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfpm_b200.so")
+# FPM_B200_LIB=check loads the bounds-checked build (make check: device asserts that
+# trap on an out-of-range index; tests/test_gpu_checked.py)
+LIB_PATH = os.path.join(_HERE, "lib", "libfpm_b200_check.so" if os.environ.get("FPM_B200_LIB") == "check"
+                        else "libfpm_b200.so")
 
 OK, ERR_CONFIG, ERR_DATA, ERR_UNSAFE_LAG, ERR_DOMAIN, ERR_CUDA, ERR_INTERNAL, ERR_UNSUPPORTED = range(8)
 MODE_GS, MODE_EPRY = 0, 1

@@ -548,6 +548,7 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
     a.bright = p.bright.p;
     a.seq_frame = p.seq_frame.p;
     a.tile_xy = p.tile_xy.p;
+    a.F = p.F;
     a.residuals = resid ? resid : p.resid.p;
     a.slots = p.G > 1 ? p.slots.p : nullptr;
     a.slot_begin = s0;
@@ -558,6 +559,10 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
     a.iters = r.iters;
     a.N = p.N;
     a.nslots = p.nslots;
+#if FPM_CHECK
+    // checked build self-test: a tile count of 0 makes every loop kernel's tile assert fire
+    if (const char* st = std::getenv("FPM_B200_CHECK_SELFTEST"); st && st[0] == '1') a.T = 0;
+#endif
     a.alpha = float(r.alpha);
     a.beta = float(r.beta);
     a.batch_T = p.batch_tiles > 0 ? p.batch_tiles : p.T;
@@ -1530,6 +1535,7 @@ int fpmgpu_update_step(fpmgpu_context* ctx, const fpmgpu_optical_config* cfg, fl
         a.bright = bf.p;
         a.seq_frame = sf.p;
         a.tile_xy = xy.p;
+        a.F = 1;
         a.residuals = res.p;
         a.meas_f32 = meas.p;
         a.num_slots = 1;

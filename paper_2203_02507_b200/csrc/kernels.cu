@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
         s_begin = args.slot_begin;
         s_end = args.num_slots;
     }
+    FPM_ASSERT(tile >= 0 && tile < args.T && s_begin >= 0 && s_end <= args.num_slots);
 
     // ---- per-tile setup: support mask, lattice pupil, origins, frame map, flags
     float2* canvas = args.canvas + size_t(tile) * N * N;
@@ -475,6 +476,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
             // canvas staging) are ordered before the TMA's async-proxy write
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar, kIBytes);
+            FPM_ASSERT(e.y >= 0 && e.y < L && F_s[e.y] >= 0 && (args.F == 0 || F_s[e.y] < args.F));
             tma_load_crop(I_s, &tmap, bar, txy.x, txy.y, F_s[e.y]);
         }
     };
@@ -487,6 +489,10 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
             if (!issued) issue(e);
             issued = false;
             const short2 o = O_s[e.y];
+            // the 64 x 64 disk block lies inside the tile's N x N canvas (every lattice
+            // gather and scatter below is an offset inside that block)
+            FPM_ASSERT(e.x >= 0 && e.x < args.iters && e.y >= 0 && e.y < L && o.x >= 0 && o.y >= 0 &&
+                       o.x + 64 <= N && o.y + 64 <= N);
             float2* cv = canvas + size_t(o.x) * N + o.y + cbase;
 
             // ---- gather: every disk load in flight at once (all lattice addresses lie in

@@ -1,6 +1,7 @@
 // Kernel launch interface shared by capi.cu and kernels.cu.
 #pragma once
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <cuda.h>
@@ -17,6 +18,30 @@ inline bool mid_disabled() {
 }
 
 enum { kModeGS = 0, kModeEPRY = 1 };
+
+// Checked build (make check -> lib/libfpm_b200_check.so, -DFPM_CHECK=1): every
+// kernel asserts the indices of its global and shared accesses (tile, origin,
+// frame, work item, slab row / owner, measurement slot) and traps on a
+// violation — the bounds half of compute-sanitizer's memcheck, which this GPU
+// pool does not allow (profiles/r2/compute_sanitizer_refused.txt). The
+// production build compiles the checks out.
+#ifndef FPM_CHECK
+#define FPM_CHECK 0
+#endif
+#if FPM_CHECK
+#define FPM_ASSERT(c)                                                                                     \
+    do {                                                                                                  \
+        if (!(c)) {                                                                                       \
+            printf("FPM_ASSERT %s:%d (%s) block %d thread %d\n", __FILE__, __LINE__, #c, int(blockIdx.x), \
+                   int(threadIdx.x));                                                                     \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define FPM_ASSERT(c) \
+    do {              \
+    } while (0)
+#endif
 
 // Layout of the TMA-staged 64 x 64 u16 measurement crop (n = 64 loop kernels):
 // 1 = 128B swizzle (16-byte chunk c of row r at chunk c ^ (r & 7)), 0 = row-major.
@@ -54,6 +79,7 @@ struct LoopArgs {
     int batch_T;              // tiles sharing the GPU with this launch (concurrent bands); 0 = T
     int jitter;               // > 0: race hunting, every warp sleeps 0..jitter ns per update / item
     unsigned jitter_seed;
+    int F;                    // frames in the LR stack (checked build: seq_frame bounds)
 };
 
 // Line FFTs for init_canvas / canvas_to_field (K2 / K3).

@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(kBoxThreads, 1) fpm_loop_box(const LoopArgs ar
             pos = en.y;
         }
         const short2 o = O_s[pos];
+        FPM_ASSERT(tile < args.T && pos >= 0 && pos < L && it >= 0 && it < args.iters && o.x >= 0 && o.y >= 0 &&
+                   o.x + NLR <= NC && o.y + NLR <= NC && F_s[pos] >= 0 && (args.F == 0 || F_s[pos] < args.F));
         const float2* cvc = canvas + size_t(o.x) * NC + o.y;
         float2* cv = canvas + size_t(o.x) * NC + o.y;
 

@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         if (round > 0) break;
         tile = blockIdx.x / CL;
     }
+    FPM_ASSERT(tile >= 0 && tile < args.T && rank >= 0 && rank < CL);
     float2* canvas = args.canvas + size_t(tile) * NC * NC;
     float2* pupil = args.pupils + size_t(tile) * NLR * NLR;
     const int2 txy = args.tile_xy[tile];
@@ -312,6 +313,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         if (DB && threadIdx.x == 0) mbar_arm(mbA + par, uint32_t(B) * SW * sizeof(float2));
         const int e_next = next_entry(e);
         const short2 o = O_s[pos];
+        FPM_ASSERT(pos >= 0 && pos < L && it >= 0 && it < args.iters && o.x >= 0 && o.y >= 0 && o.x + NLR <= NC &&
+                   o.y + NLR <= NC && (args.F == 0 || F_s[pos] < args.F));
         float2* cv = canvas + size_t(o.x) * NC + o.y;
         // box rows are owned by canvas row (o.x + i) mod CL: a CTA reads in phase A only
         // canvas rows it wrote itself in earlier phases C, so consecutive updates need no
@@ -404,9 +407,11 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 }
             }
             F.fA(x);  // S keeps conj(IFFT_rows(g)): phase B's forward column FFT undoes it
+            FPM_ASSERT(i >= b0 && i < b0 + B);
 #pragma unroll
             for (int r = 0; r < M; ++r) {
                 const int col = F.a_out(r), owner = col / SW;
+                FPM_ASSERT(col >= 0 && col < NLR && owner >= 0 && owner < CL);
                 if constexpr (DB) {
                     const uint32_t off = uint32_t((size_t(i - b0) * RS + (col - owner * SW)) * sizeof(float2));
                     st_async_f2(map_rank(smem_addr(S) + off, owner), x[r], map_rank(smem_addr(mbA + par), owner));
@@ -450,6 +455,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int row = F.scr(k0);
+                FPM_ASSERT(row >= 0 && row < NLR && (Ic - I_s) + row * SW < SW * NLR);
                 const float Iv = float(Ic[row * SW]);
                 den += Iv;
                 // |e| = 0 rule (recon.cpp:122) as in fpm_loop64: Re nudged by sgn 2^-60 maps
@@ -534,6 +540,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
 #pragma unroll
             for (int m = 0; m < M; ++m) {
                 const int col = F.c_in(m), owner = col / SW;
+                FPM_ASSERT(col >= 0 && col < NLR && owner >= 0 && owner < CL && i >= b0 && i < b0 + B);
                 x[m] = cluster.map_shared_rank(S, owner)[size_t(i - b0) * RS + (col - owner * SW)];
             }
             F.fC(x);

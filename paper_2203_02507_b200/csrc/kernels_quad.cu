@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
         s_begin = args.slot_begin;
         s_end = args.num_slots;
     }
+    FPM_ASSERT(tile >= 0 && tile < args.T && s_begin >= 0 && s_end <= args.num_slots);
 
     // ---- per-tile setup: support mask, lattice pupil, origins, frame map, flags
     float2* canvas = args.canvas + size_t(tile) * N * N;
@@ -340,6 +341,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
         if (t == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar, kQIBytes);
+            FPM_ASSERT(led >= 0 && led < L && F_s[led] >= 0 && (args.F == 0 || F_s[led] < args.F));
             tma_load_crop(I_s, &tmap, bar, txy.x, txy.y, F_s[led]);
         }
     };
@@ -349,6 +351,8 @@ __global__ void __launch_bounds__(kQThreads, MINB)
         if (!issued) issue(c_pos);
         issued = false;
         const short2 o = O_s[c_pos];
+        FPM_ASSERT(c_pos >= 0 && c_pos < L && c_it >= 0 && c_it < args.iters && o.x >= 0 && o.y >= 0 &&
+                   o.x + 64 <= N && o.y + 64 <= N);
         float2* cv = canvas + size_t(o.x) * N + o.y + cbase;
 
         // ---- gather the disk x P' (conjugated: the IFFT runs as conj(FFT(conj x)))
