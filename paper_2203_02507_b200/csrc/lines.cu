@@ -137,10 +137,12 @@ __global__ void __launch_bounds__(256) lines_fft(const LinesArgs a) {
 // lane-strided reads and the digit-reversed writes of F1).
 template <int WHICH>
 __global__ void __launch_bounds__(512) lines_fft_w256(const LinesArgs a) {
-    constexpr int NL = 256, LPB = 16, M = 8, LS = NL + NL / 32;
+    constexpr int NL = 256, LPB = 16, M = 8, LS = NL + NL / 32 + 1;  // odd in float2 pairs: column phases conflict-free
     constexpr bool INV = WHICH >= 2;
     constexpr bool COLS = (WHICH & 1) == 1;
     __shared__ float2 s[LPB * LS];
+    __shared__ float2 tw_s[NL];  // the twiddle table, staged once per block (the warp FFTs' per-lane constants)
+    for (int k = threadIdx.x; k < NL; k += blockDim.x) tw_s[k] = a.tw[k];
     const int tile = blockIdx.y;
     const int l0 = blockIdx.x * LPB;
     const size_t base = size_t(tile) * NL * NL;
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(512) lines_fft_w256(const LinesArgs a) {
     __syncthreads();
     {
         WarpFFT<M> F;
-        F.init_table(l, NL, a.tw);
+        F.init_smem(l, NL, tw_s);
         float2* ln = s + w * LS;
         float2 x[M];
 #pragma unroll
@@ -278,10 +280,12 @@ __device__ __forceinline__ float seed_bilinear(const LinesArgs& a, int tile, int
 #endif
 template <int WHICH>
 __global__ void __launch_bounds__(512, FPM_LINES_BOX_MINB) lines_box_w256(const LinesArgs a) {
-    constexpr int NL = 256, LPB = 16, M = 8, LS = NL + NL / 32;
+    constexpr int NL = 256, LPB = 16, M = 8, LS = NL + NL / 32 + 1;  // odd in float2 pairs: column phases conflict-free
     constexpr bool INV = WHICH >= 2;
     constexpr bool COLS = (WHICH & 1) == 1;
     __shared__ float2 s[LPB * LS];
+    __shared__ float2 tw_s[NL];  // the twiddle table, staged once per block (the warp FFTs' per-lane constants)
+    for (int k = threadIdx.x; k < NL; k += blockDim.x) tw_s[k] = a.tw[k];
     const int tile = blockIdx.y;
     const int b0 = a.box0, bn = a.boxn;
     const int l0 = (WHICH == 1 || WHICH == 2 ? b0 : 0) + blockIdx.x * LPB;  // first line of the block
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(512, FPM_LINES_BOX_MINB) lines_box_w256(const 
     __syncthreads();
     {
         WarpFFT<M> F;
-        F.init_table(l, NL, a.tw);
+        F.init_smem(l, NL, tw_s);
         float2* ln = s + w * LS;
         float2 x[M];
 #pragma unroll
@@ -441,6 +445,8 @@ __global__ void __launch_bounds__(512, FPM_LINES_BOX_MINB) lines_box_w256(const 
 __global__ void __launch_bounds__(512) lines_box_init_rows(const LinesArgs a) {
     constexpr int NL = 256, RB = 32, MAXLR = 16, M = 8, LS = NL + NL / 32;
     __shared__ float2 s[MAXLR * LS];
+    __shared__ float2 tw_s[NL];
+    for (int k = threadIdx.x; k < NL; k += blockDim.x) tw_s[k] = a.tw[k];
     const int tile = blockIdx.y, i0 = blockIdx.x * RB;
     const int b0 = a.box0, bn = a.boxn, n = a.n, up = a.up;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -464,7 +470,7 @@ __global__ void __launch_bounds__(512) lines_box_init_rows(const LinesArgs a) {
     __syncthreads();
     if (w < ny) {
         WarpFFT<M> F;
-        F.init_table(l, NL, a.tw);
+        F.init_smem(l, NL, tw_s);
         float2* ln = s + w * LS;
         float2 x[M];
 #pragma unroll

@@ -104,6 +104,25 @@ struct WarpFFT {
             tw[k0] = make_float4(w.x, w.y, -w.y, w.x);
         }
     }
+    // the same from a copy of the table in shared memory (plain loads)
+    __device__ void init_smem(int l, int n, const float2* tab) {
+        lb = M * brev5(l);
+        ln = l;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const int h = 1 << k;
+            const bool up = (l & h) != 0;
+            const float2 w = up ? tab[(l & (h - 1)) * (n / (2 * h))] : make_float2(1.f, 0.f);
+            cw[k] = make_float4(w.x, w.y, -w.y, w.x);
+            sgk[k] = up ? -1.f : 1.f;
+        }
+        mi = (l & 3) == 3;
+#pragma unroll
+        for (int k0 = 0; k0 < M; ++k0) {
+            const float2 w = tab[(l * k0) % n];
+            tw[k0] = make_float4(w.x, w.y, -w.y, w.x);
+        }
+    }
     static __device__ __forceinline__ float2 mul(float2 v, const float4& w) {
         return cmul_sw(v, make_float2(w.x, w.y), make_float2(w.z, w.w));
     }
