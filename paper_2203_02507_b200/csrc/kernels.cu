@@ -52,6 +52,12 @@ constexpr int kGroupThreads = 128;
 // at the scatter, the next crop's TMA issued at that barrier (measured 31.74 vs 31.17 ms)
 #define FPM_O_STAGE 0
 #endif
+#ifndef FPM_TMA_LANE
+#define FPM_TMA_LANE 32  // thread (of the group) that issues the measurement TMA (0: 30.28, 32: 30.18 ms)
+#endif
+#ifndef FPM_SUM_LANE
+#define FPM_SUM_LANE 0  // thread (of the group) that adds the update's residual ratio
+#endif
 #ifndef FPM_O_EARLY
 #define FPM_O_EARLY 1  // 1: the scatter's old canvas values loaded before pass 1's step 2 (loop 30.455 vs 30.57 ms; before the alternating transposes 31.24 vs 31.16)
 #endif
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     bool issued = false;
     bool pupil_dirty = true;  // EPRY: max|P|^2 changes only after a pupil step
     auto issue = [&](int2 e) {
-        if (MEAS == kMeasTMA && tl == 0) {
+        if (MEAS == kMeasTMA && tl == FPM_TMA_LANE) {
             // the staging buffer's earlier generic-proxy accesses (modulus reads, the EPRY
             // canvas staging) are ordered before the TMA's async-proxy write
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -629,7 +635,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                     issued = true;
                 }
             }
-            if (tl == 0) {
+            if (tl == FPM_SUM_LANE) {
                 const float nsum = (rg[0] + rg[1]) + (rg[2] + rg[3]);
                 float dsum;
                 if (first) {
