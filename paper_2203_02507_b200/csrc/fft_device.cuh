@@ -60,6 +60,12 @@ __device__ __forceinline__ float2 cmul_sw(float2 v, float2 w, float2 wsw) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(make_float2(v.y, v.y))), "l"(pk(wsw)), "l"(t));
     return upk(r);
 }
+// v * w in two packed instructions from w alone: FMUL2 t = v w.y, then FFMA2 v w.x +
+// (-t.y, t.x) (the half swap and the partial negation are operand modifiers)
+__device__ __forceinline__ float2 cmul2(float2 v, float2 w) {
+    const float2 t = cscale(v, w.y);
+    return cfma(w.x, v, make_float2(-t.y, t.x));
+}
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }

@@ -34,6 +34,15 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef FPM_CL_ASY256
+#define FPM_CL_ASY256 0  // n = 256, one slab buffer: phase-A rows by st.async counted on an mbarrier
+#endif
+#ifndef FPM_CL_SPLIT
+#define FPM_CL_SPLIT 0  // n = 256: first-row loads between barrier.cluster.arrive and wait
+#endif
+#ifndef FPM_CL_GATE
+#define FPM_CL_GATE 0  // EPRY maxima only when needed (bright update / pupil changed)
+#endif
 #ifndef FPM_CL_DB256
 #define FPM_CL_DB256 0  // n = 256 on 8-CTA clusters: double-buffered slabs (st.async + mbarrier, no end-of-update barrier)
 #endif
@@ -88,6 +97,13 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
                  "l"(gsrc)
                  : "memory");
 }
+__device__ __forceinline__ void cluster_arrive_release() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_sync_relaxed() {
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
@@ -143,6 +159,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
     // DB: two slab / reduction buffers used alternately, so an update's phase A never
     // overwrites what the previous update's phase C still reads: no end-of-update barrier
     constexpr bool DB = NLR <= 128 || (FPM_CL_DB256 && NLR == 256 && CL >= 8);
+    constexpr bool ASY = DB || (FPM_CL_ASY256 && NLR == 256);  // phase-A sends by st.async + mbarrier
+    constexpr bool SPLIT = FPM_CL_SPLIT && NLR == 256 && !DB;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = int(cluster.block_rank());
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -194,7 +212,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
     FFT F;
     F.init(l, NLR, TB);
     const float inv_n2 = 1.0f / float(NLR * NLR);
-    if (DB && threadIdx.x == 0) {
+    if (ASY && threadIdx.x == 0) {
         mbar_init1(mbA);
         mbar_init1(mbA + 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -298,11 +316,14 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         }
     };
     int e = next_entry((queue ? it_q * L : args.slot_begin * G) - 1);
+    bool pdirty = true;  // GATE: max|P|^2 changes only after a pupil step
     if (e >= 0) {
         int it0, pos0;
         entry_at(e, it0, pos0);
         stage(pos0);
     }
+    float2 Oa[M], Pa[M];  // phase-A prefetch (SPLIT: loaded under the previous update's end barrier)
+    bool a_loaded = false;
     for (; e >= 0;) {
         jitter_sleep<JIT>(args, e);
         int it, pos;
@@ -310,7 +331,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         float2* const S = par ? S1 : S0;
         float* const wred = par ? wred1 : wred0;
         // DB: this update's slab arrives by st.async, counted on mbA[par] (B rows x SW columns)
-        if (DB && threadIdx.x == 0) mbar_arm(mbA + par, uint32_t(B) * SW * sizeof(float2));
+        if (ASY && threadIdx.x == 0) mbar_arm(mbA + par, uint32_t(B) * SW * sizeof(float2));
         const int e_next = next_entry(e);
         const short2 o = O_s[pos];
         FPM_ASSERT(pos >= 0 && pos < L && it >= 0 && it < args.iters && o.x >= 0 && o.y >= 0 && o.x + NLR <= NC &&
@@ -320,22 +341,25 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         // canvas rows it wrote itself in earlier phases C, so consecutive updates need no
         // cross-CTA ordering of canvas memory (the disk moves with the LED)
         const int rfirst = b0 + ((rank - (int(o.x) + b0) % CL) % CL + CL) % CL;
+        const bool bright = MODE == kModeEPRY && B_s[pos] != 0;
+        const bool want_o = MODE == kModeEPRY && (bright || !FPM_CL_GATE);
+        const bool want_p = MODE == kModeEPRY && (pdirty || !FPM_CL_GATE);
 
         // ---- A: IFFT of this CTA's box rows, outputs to the column owners
         // the disk loads of a warp's next row are issued before the current row's FFT
         // (n <= 128; the n = 256 kernel has no register room for a second row)
         float omax = 0.f, pmax = 0.f;
-        float2 Oa[M], Pa[M];
-        auto load_row = [&](int ii) {
+        auto load_row_at = [&](const float2* cvp, int ii) {
             const short2 run = SR[ii];
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int c = F.a_in(k0);
                 const bool on = FFT::live(k0) && c >= run.x && c < run.y;
-                Oa[k0] = on ? cv[size_t(ii) * NC + c] : make_float2(0.f, 0.f);
+                Oa[k0] = on ? cvp[size_t(ii) * NC + c] : make_float2(0.f, 0.f);
                 Pa[k0] = on ? pupil[ii * NLR + c] : make_float2(0.f, 0.f);
             }
         };
+        auto load_row = [&](int ii) { load_row_at(cv, ii); };
         // n = 256: the warp's next box row (canvas and pupil over the box columns) is staged
         // into its row buffer by cp.async while the current row transforms; slot x ^ ((x >> 4) & 15)
         // makes the gather's stride-8 reads conflict-free (a half-warp's stride-16 columns land
@@ -349,7 +373,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             cp_async_commit();
         };
         const int i0 = rfirst + CL * w;
-        if (PF && i0 < b0 + B) load_row(i0);
+        if (PF && i0 < b0 + B && !a_loaded) load_row(i0);
+        a_loaded = false;
         if (STG && i0 < b0 + B) stage_row(i0);
         for (int i = i0; i < b0 + B; i += CL * NW) {
             float2 x[M];
@@ -359,10 +384,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                     const int c = F.a_in(k0);
                     const float2 g = cmul(Oa[k0], Pa[k0]);  // conj, signed: the row IFFT runs as conj(FFT(conj g))
                     x[k0] = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
-                    if (MODE == kModeEPRY) {
-                        omax = fmaxf(omax, cabs2(Oa[k0]));
-                        pmax = fmaxf(pmax, cabs2(Pa[k0]));
-                    }
+                    if (want_o) omax = fmaxf(omax, cabs2(Oa[k0]));
+                    if (want_p) pmax = fmaxf(pmax, cabs2(Pa[k0]));
                 }
                 if (i + CL * NW < b0 + B) load_row(i + CL * NW);
             } else if constexpr (STG) {
@@ -378,10 +401,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                         const float2 P = RB[RBW + rb_slot(c - b0)];
                         const float2 g = cmul(O, P);
                         v = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
-                        if (MODE == kModeEPRY) {
-                            omax = fmaxf(omax, cabs2(O));
-                            pmax = fmaxf(pmax, cabs2(P));
-                        }
+                        if (want_o) omax = fmaxf(omax, cabs2(O));
+                        if (want_p) pmax = fmaxf(pmax, cabs2(P));
                     }
                     x[k0] = v;
                 }
@@ -398,10 +419,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                         const float2 P = pupil[i * NLR + c];
                         const float2 g = cmul(O, P);
                         v = ((i + c) & 1) ? make_float2(-g.x, g.y) : make_float2(g.x, -g.y);
-                        if (MODE == kModeEPRY) {
-                            omax = fmaxf(omax, cabs2(O));
-                            pmax = fmaxf(pmax, cabs2(P));
-                        }
+                        if (want_o) omax = fmaxf(omax, cabs2(O));
+                        if (want_p) pmax = fmaxf(pmax, cabs2(P));
                     }
                     x[k0] = v;
                 }
@@ -412,7 +431,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             for (int r = 0; r < M; ++r) {
                 const int col = F.a_out(r), owner = col / SW;
                 FPM_ASSERT(col >= 0 && col < NLR && owner >= 0 && owner < CL);
-                if constexpr (DB) {
+                if constexpr (ASY) {
                     const uint32_t off = uint32_t((size_t(i - b0) * RS + (col - owner * SW)) * sizeof(float2));
                     st_async_f2(map_rank(smem_addr(S) + off, owner), x[r], map_rank(smem_addr(mbA + par), owner));
                 } else {
@@ -432,9 +451,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             }
         }
         cp_async_wait_all();  // this thread's part of the measurement slab has landed
-        if constexpr (DB) {
+        if constexpr (ASY) {
             __syncthreads();  // measurement slab and the EPRY partials visible CTA-wide
-            mbar_wait_parity(mbA + par, (nupd >> 1) & 1u);  // every column of every box row landed
+            // every column of every box row landed (mbA[par]'s phase; DB alternates two barriers)
+            mbar_wait_parity(mbA + par, DB ? (nupd >> 1) & 1u : nupd & 1u);
         } else {
             cluster.sync();
         }
@@ -486,7 +506,25 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             wred[w * 4] = num;
             wred[w * 4 + 1] = den;
         }
-        cluster.sync();
+        float2 Pc[PFC ? M : 1], Oc[PFC ? M : 1];
+        auto load_c = [&](int ii) {
+            const short2 run = SR[ii];
+#pragma unroll
+            for (int k0 = 0; k0 < M; ++k0) {
+                const int c = F.c_out(k0);
+                const bool on = FFT::live(k0) && c >= run.x && c < run.y;
+                Pc[k0] = on ? pupil[ii * NLR + c] : make_float2(0.f, 0.f);
+                Oc[k0] = (MODE == kModeEPRY && on) ? cv[size_t(ii) * NC + c] : make_float2(0.f, 0.f);
+            }
+        };
+        const int ic0 = rfirst + CL * w;
+        if constexpr (SPLIT) {  // the first phase-C row's operands load while other CTAs finish B
+            cluster_arrive_release();
+            if (PFC && ic0 < b0 + B) load_c(ic0);
+            cluster_wait();
+        } else {
+            cluster.sync();
+        }
         if (e_next >= 0) {  // the slab is free: stage the next update's measurement under phase C
             int itn, posn;
             entry_at(e_next, itn, posn);
@@ -514,27 +552,18 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             }
             if (l == 0) {
                 if (rank == 0) stage_sum[it] += a1 > 0.f ? double(__fdividef(a0, a1)) : 0.0;  // as fpm_loop64
-                upd[0] = (a2 > 0.f && B_s[pos]) ? args.beta / a2 : 0.f;  // bright-field pupil steps only
-                upd[1] = a3 > 0.f ? args.alpha / a3 : 0.f;
+                upd[0] = (a2 > 0.f && bright) ? args.beta / a2 : 0.f;  // bright-field pupil steps only
+                if (want_p) upd[1] = a3 > 0.f ? args.alpha / a3 : 0.f;  // else the pupil's value stands
             }
         }
         __syncthreads();
         const float inv_omax = upd[0], inv_pmax = upd[1];
 
         // ---- C: FFT of this CTA's box rows (fetched from the column slabs), scatter
-        for (int i = rfirst + CL * w; i < b0 + B; i += CL * NW) {
+        for (int i = ic0; i < b0 + B; i += CL * NW) {
             // the scatter's disk operands are loaded first, their latency under the FFT
             const short2 run = SR[i];
-            float2 Pc[PFC ? M : 1], Oc[PFC ? M : 1];
-            if constexpr (PFC) {
-#pragma unroll
-                for (int k0 = 0; k0 < M; ++k0) {
-                    const int c = F.c_out(k0);
-                    const bool on = FFT::live(k0) && c >= run.x && c < run.y;
-                    Pc[k0] = on ? pupil[i * NLR + c] : make_float2(0.f, 0.f);
-                    Oc[k0] = (MODE == kModeEPRY && on) ? cv[size_t(i) * NC + c] : make_float2(0.f, 0.f);
-                }
-            }
+            if (PFC && !(SPLIT && i == ic0)) load_c(i);
             if constexpr (STG && FPM_CL_STAGE_C) stage_row(i);  // the row's canvas and pupil, under its FFT
             float2 x[M];
 #pragma unroll
@@ -580,8 +609,24 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             cluster.sync();
         } else {
             __syncthreads();  // a canvas row's next reader may be another warp of this CTA
-            if (!DB) cluster_sync_relaxed();  // single slab buffer: phase C reads done
+            if constexpr (SPLIT) {  // the next update's first phase-A row loads under the barrier
+                cluster_arrive_relaxed();
+                if (PF && e_next >= 0) {
+                    int itn, posn;
+                    entry_at(e_next, itn, posn);
+                    const short2 on_ = O_s[posn];
+                    const int rf = b0 + ((rank - (int(on_.x) + b0) % CL) % CL + CL) % CL;
+                    if (rf + CL * w < b0 + B) {
+                        load_row_at(canvas + size_t(on_.x) * NC + on_.y, rf + CL * w);
+                        a_loaded = true;
+                    }
+                }
+                cluster_wait();
+            } else if (!DB) {
+                cluster_sync_relaxed();  // single slab buffer: phase C reads done
+            }
         }
+        pdirty = MODE == kModeEPRY && inv_omax > 0.f;
         par ^= DB ? 1 : 0;
         ++nupd;
         e = e_next;

@@ -206,7 +206,7 @@ __device__ __forceinline__ float2 rot_g(float2 x, float a, float2 bb) {
 template <bool MID>
 struct WarpFFT256 {
     static constexpr int kBufFloat2 = 16 * 17;  // per-warp transpose buffer (row stride 17: conflict-free)
-    float4 tw[8];
+    float2 tw[8];  // two registers each: cmul2 needs no pre-swapped copy
     float ga[8];         // cos(2 pi k / 16) on the upper half (h = 1), 1 on the lower
     float2 gb[8];        // (sin, -sin)(2 pi k / 16) on the upper half, 0 on the lower
     float sg;            // +1 lower half, -1 upper
@@ -239,12 +239,10 @@ struct WarpFFT256 {
             ga[k] = h ? float(c) : 1.f;
             gb[k] = h ? make_float2(float(s), -float(s)) : make_float2(0.f, 0.f);
             sincospi(-2.0 * double((p * (2 * k + h)) & 255) / 256.0, &s, &c);
-            tw[k] = make_float4(float(c), float(s), -float(s), float(c));
+            tw[k] = make_float2(float(c), float(s));
         }
     }
-    static __device__ __forceinline__ float2 mul(float2 v, const float4& w) {
-        return cmul_sw(v, make_float2(w.x, w.y), make_float2(w.z, w.w));
-    }
+    static __device__ __forceinline__ float2 mul(float2 v, float2 w) { return cmul2(v, w); }
     // DFT16 over the pair, decimation in time: lower lane holds the even inputs,
     // upper the odd ones (register a = input 2a + h); out: register k = X[k + 8 h]
     template <bool PIN>
