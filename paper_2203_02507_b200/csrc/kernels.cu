@@ -43,6 +43,20 @@ constexpr int kIBytes = 64 * 64 * 2;            // staged u16 measurement, TMA 1
 constexpr int kTBytes = 64 * 64 * 8;            // transpose buffer (swizzled, unpadded)
 constexpr int kGroupBytes = kIBytes + kTBytes;  // 40 KB, a multiple of 1 KB
 constexpr int kGroupThreads = 128;
+
+#if FPM_TW2
+using TwEntry = float2;
+__device__ __forceinline__ float2 tw_mul(float2 v, float2 w) { return cmul2(v, w); }
+__device__ __forceinline__ float2 tw_entry(double c, double s) { return make_float2(float(c), float(s)); }
+#else
+using TwEntry = float4;
+__device__ __forceinline__ float2 tw_mul(float2 v, float4 w) {
+    return cmul_sw(v, make_float2(w.x, w.y), make_float2(w.z, w.w));
+}
+__device__ __forceinline__ float4 tw_entry(double c, double s) {
+    return make_float4(float(c), float(s), -float(s), float(c));
+}
+#endif
 #ifndef FPM_PAIR_ROT
 #define FPM_PAIR_ROT 1  // step-1 pair twiddles W8^1, W8^3 as rotations (scale folded into the column twiddles)
 #endif
@@ -57,6 +71,9 @@ constexpr int kGroupThreads = 128;
 #endif
 #ifndef FPM_SUM_LANE
 #define FPM_SUM_LANE 0  // thread (of the group) that adds the update's residual ratio
+#endif
+#ifndef FPM_TW2
+#define FPM_TW2 1  // twiddle tables as float2 with the two-instruction cmul2 (0: float4 (w, iw) pairs, cmul_sw)
 #endif
 #ifndef FPM_O_EARLY
 #define FPM_O_EARLY 1  // 1: the scatter's old canvas values loaded before pass 1's step 2 (loop 30.455 vs 30.57 ms; before the alternating transposes 31.24 vs 31.16)
@@ -113,7 +130,7 @@ __device__ __forceinline__ int tswz(int pp) {
 // pending read, so the transposes need only their write-to-read barriers (the
 // barrier after the modulus is gone; the modulus's reductions and the measurement
 // buffer are released by pass 1's transpose barrier).
-__device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const float4* W4_s, int p, int h,
+__device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const TwEntry* W4_s, int p, int h,
                                           float sg, const float2 (&tw)[4], const float2 (&twsw)[4], float kh,
                                           float c1, float c3, bool skip_cols, bool layout_b) {
     const int tr = p >> 3, tc = p & 7;
@@ -193,16 +210,16 @@ __device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const 
     // twiddle W64^(n0r k0r + n0c k0c), k0 = (a, 4h + m); table entries (w, (-w.y, w.x))
 #pragma unroll
     for (int a = 1; a < 8; ++a) {
-        const float4 w = W4_s[(tr * a) & 63];
+        const TwEntry w = W4_s[(tr * a) & 63];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) v[a][m] = cmul_sw(v[a][m], make_float2(w.x, w.y), make_float2(w.z, w.w));
+        for (int m = 0; m < 4; ++m) v[a][m] = tw_mul(v[a][m], w);
     }
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         // = W64^(tc (4h + m)), in lane order; [128, 192): the same without the pair trick's scale
-        const float4 w = W4_s[((FPM_P0_INPUT_SWAP && skip_cols) ? 128 : 64) + m * 16 + 2 * tc + h];
+        const TwEntry w = W4_s[((FPM_P0_INPUT_SWAP && skip_cols) ? 128 : 64) + m * 16 + 2 * tc + h];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) v[a][m] = cmul_sw(v[a][m], make_float2(w.x, w.y), make_float2(w.z, w.w));
+        for (int a = 0; a < 8; ++a) v[a][m] = tw_mul(v[a][m], w);
     }
     if (!layout_b) {
         // layout A: element k0 = (a, 4h + m) of residue p goes to row p' = 8a + 4h + m, slot p
@@ -280,7 +297,7 @@ __device__ __forceinline__ void fft_second(float2 (&v)[8][4], const float2* T_s,
         for (int i = 0; i < 4; ++i) v[a][i] = cfma(sg, v[a][i], shfl_pair(v[a][i]));  // y_i + y_(i+4) | y_i - y_(i+4)
 #pragma unroll
         for (int i = 1; i < 4; ++i)
-            v[a][i] = i == 2 ? mul_mi_odd(v[a][i], h) : cmul_sw(v[a][i], tw[i], twsw[i]);
+            v[a][i] = i == 2 ? mul_mi_odd(v[a][i], h) : (FPM_TW2 ? cmul2(v[a][i], tw[i]) : cmul_sw(v[a][i], tw[i], twsw[i]));
         if (skip_rows)  // the scatter reads columns j in {1, 2} of these rows only
             dft4_o12<false>(v[a][0], v[a][1], v[a][2], v[a][3]);
         else
@@ -345,8 +362,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
     off += size_t(NP) * kGroupThreads * sizeof(float2);
     // [0, 64): (W64^m, swizzled), m in [0, 64); [64, 128): the column twiddle W64^(tc (4h + m))
     // at 64 + 16 m + 2 tc + h, i.e. in lane order (lane = 2 (8 tr + tc) + h): conflict-free
-    float4* W4_s = reinterpret_cast<float4*>(smem + off);
-    off += 192 * sizeof(float4);
+    TwEntry* W4_s = reinterpret_cast<TwEntry*>(smem + off);
+    off += 192 * sizeof(float4);  // (sized for the float4 entries of FPM_TW2 = 0)
     double* stage_sum = reinterpret_cast<double*>(smem + off);
     off += size_t(args.iters) * sizeof(double);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off);
@@ -378,7 +395,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
         // column twiddles of the even lane for m = 1, 3 carry the pair combine's +-1/sqrt(2)
         const double f = (FPM_PAIR_ROT && t >= 64 && t < 128 && (e & 1) == 0 && ((e >> 4) & 1))
                              ? ((e >> 4) == 1 ? 1.0 : -1.0) * 0.70710678118654752440 : 1.0;
-        W4_s[t] = make_float4(float(c * f), float(s * f), -float(s * f), float(c * f));
+        W4_s[t] = tw_entry(c * f, s * f);
     }
     // pair-combine twiddles W8^m, m = 1..3, on the odd lane (1 on the even lane)
     float2 tw[4];
