@@ -102,7 +102,7 @@ __device__ __forceinline__ void dif_pair(float2& x0, float2& x1, float2& x2, flo
 // PIN: only i, j in {1, 2} hold data on entry (the disk block of the IFFT);
 // POUT: only outputs i, j in {1, 2} are formed (the disk the scatter reads).
 template <bool PIN, bool POUT>
-__device__ __forceinline__ void fft64x64_quad(float2 (&v)[4][4], float2* T_s, const float4* Wr_s, const float4* Wc_s,
+__device__ __forceinline__ void fft64x64_quad(float2 (&v)[4][4], float2* T_s, const float2* Wr_s, const float2* Wc_s,
                                               int t, int tr, int tc, const PairK& kr, const PairK& kc) {
     // ---- step 1 rows: DFT4 over i (n1r = 2i + hr) per column, pair over hr
 #pragma unroll
@@ -127,15 +127,15 @@ __device__ __forceinline__ void fft64x64_quad(float2 (&v)[4][4], float2* T_s, co
     // even lanes' deferred +-1/sqrt(2); entries (w, (-w.y, w.x))
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        const float4 w = Wr_s[(m * 2 + kr.h) * 8 + tr];
+        const float2 w = Wr_s[(m * 2 + kr.h) * 8 + tr];
 #pragma unroll
-        for (int n = 0; n < 4; ++n) v[m][n] = cmul_sw(v[m][n], make_float2(w.x, w.y), make_float2(w.z, w.w));
+        for (int n = 0; n < 4; ++n) v[m][n] = cmul2(v[m][n], w);
     }
 #pragma unroll
     for (int n = 0; n < 4; ++n) {
-        const float4 w = Wc_s[n * 16 + tc * 2 + kc.h];
+        const float2 w = Wc_s[n * 16 + tc * 2 + kc.h];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) v[m][n] = cmul_sw(v[m][n], make_float2(w.x, w.y), make_float2(w.z, w.w));
+        for (int m = 0; m < 4; ++m) v[m][n] = cmul2(v[m][n], w);
     }
     // ---- transpose: element (k0r, k0c) of residue p = 8tr + tc -> row 8k0r + k0c, slot
     // tswz_q(k0r, k0c, p) = p ^ 2k0c ^ 4(k0r >> 2) ^ 8(p >> 5): every half-warp of a 64-bit
@@ -218,8 +218,8 @@ __global__ void __launch_bounds__(kQThreads, MINB)
     size_t off = kQIBytes + kQTBytes;
     float2* P_s = reinterpret_cast<float2*>(smem + off);  // [NP][256], P' = (-1)^(i+j) P, 0 off the support
     off += size_t(kQNP) * kQThreads * sizeof(float2);
-    float4* Wr_s = reinterpret_cast<float4*>(smem + off);  // [m][hr][tr]: W64^(tr (4hr + m)), pre-scaled
-    float4* Wc_s = Wr_s + 64;                              // [n][tc][hc]: W64^(tc (4hc + n)), pre-scaled
+    float2* Wr_s = reinterpret_cast<float2*>(smem + off);  // [m][hr][tr]: W64^(tr (4hr + m)), pre-scaled
+    float2* Wc_s = Wr_s + 64;                              // [n][tc][hc]: W64^(tc (4hc + n)), pre-scaled
     off += 128 * sizeof(float4);
     double* stage_sum = reinterpret_cast<double*>(smem + off);
     off += size_t(args.iters) * sizeof(double);
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
         double s, c;
         sincospi(-double(ex) / 32.0, &s, &c);
         const double f = (h == 0 && (m & 1)) ? (m == 1 ? 0.70710678118654752440 : -0.70710678118654752440) : 1.0;
-        Wr_s[t] = make_float4(float(c * f), float(s * f), -float(s * f), float(c * f));
+        Wr_s[t] = make_float2(float(c * f), float(s * f));  // float2 entries: cmul2
     }
     const PairK kr = pair_k(hr), kc = pair_k(hc);
     if (t == 0) {

@@ -32,17 +32,17 @@ __device__ __forceinline__ void dftM(float2 (&x)[M]) {
     }
 }
 
-// Per-lane constants of the warp FFTs, as (w, (-w.y, w.x)) pairs for the packed
-// two-instruction complex multiply: cw[k] = W_(2h)^(l mod h) on the upper lane
+// Per-lane constants of the warp FFTs (float2; cmul2 multiplies in two packed
+// instructions without a pre-swapped copy): cw[k] = W_(2h)^(l mod h) on the upper lane
 // of the stage h = 2^k (1 on the lower lane), sgk[k] = -1 on the upper lane;
 // tw[k0] = W_n^(l k0). Forward transforms only: an inverse is run as
 // conj(FFT(conj x)), the conjugations folded into the callers' loads and stores.
 template <int M>
 struct WarpFFT {
     static constexpr int kBufFloat2 = 0;  // no shared-memory transpose
-    float4 cw[5];  // cw[0] = 1 and cw[1] in {1, -i} are applied without multiplies (stage())
+    float2 cw[5];  // cw[0] = 1 and cw[1] in {1, -i} are applied without multiplies (stage())
     float sgk[5];
-    float4 tw[M];
+    float2 tw[M];
     bool mi = false;  // lane of stage h = 2 whose twiddle is -i ((l & 3) == 3)
     int lb = 0;       // M br5(l)
     int ln = 0;       // l
@@ -74,7 +74,7 @@ struct WarpFFT {
             double s, c;
             sincospi(-double(l & (h - 1)) / double(h), &s, &c);
             const float wc = up ? float(c) : 1.f, ws = up ? float(s) : 0.f;
-            cw[k] = make_float4(wc, ws, -ws, wc);
+            cw[k] = make_float2(wc, ws);
             sgk[k] = up ? -1.f : 1.f;
         }
         mi = (l & 3) == 3;
@@ -82,7 +82,7 @@ struct WarpFFT {
         for (int k0 = 0; k0 < M; ++k0) {
             double s, c;
             sincospi(-2.0 * double(l * k0) / double(n), &s, &c);
-            tw[k0] = make_float4(float(c), float(s), -float(s), float(c));
+            tw[k0] = make_float2(float(c), float(s));
         }
     }
     // the same constants from a table tab[m] = W_n^m (m in [0, n)) in global memory
@@ -94,14 +94,14 @@ struct WarpFFT {
             const int h = 1 << k;
             const bool up = (l & h) != 0;
             const float2 w = up ? __ldg(tab + (l & (h - 1)) * (n / (2 * h))) : make_float2(1.f, 0.f);
-            cw[k] = make_float4(w.x, w.y, -w.y, w.x);
+            cw[k] = w;
             sgk[k] = up ? -1.f : 1.f;
         }
         mi = (l & 3) == 3;
 #pragma unroll
         for (int k0 = 0; k0 < M; ++k0) {
             const float2 w = __ldg(tab + (l * k0) % n);
-            tw[k0] = make_float4(w.x, w.y, -w.y, w.x);
+            tw[k0] = w;
         }
     }
     // the same from a copy of the table in shared memory (plain loads)
@@ -113,19 +113,17 @@ struct WarpFFT {
             const int h = 1 << k;
             const bool up = (l & h) != 0;
             const float2 w = up ? tab[(l & (h - 1)) * (n / (2 * h))] : make_float2(1.f, 0.f);
-            cw[k] = make_float4(w.x, w.y, -w.y, w.x);
+            cw[k] = w;
             sgk[k] = up ? -1.f : 1.f;
         }
         mi = (l & 3) == 3;
 #pragma unroll
         for (int k0 = 0; k0 < M; ++k0) {
             const float2 w = tab[(l * k0) % n];
-            tw[k0] = make_float4(w.x, w.y, -w.y, w.x);
+            tw[k0] = w;
         }
     }
-    static __device__ __forceinline__ float2 mul(float2 v, const float4& w) {
-        return cmul_sw(v, make_float2(w.x, w.y), make_float2(w.z, w.w));
-    }
+    static __device__ __forceinline__ float2 mul(float2 v, float2 w) { return cmul2(v, w); }
     // lane twiddle of stage k: W_2^0 = 1 (none), W_4^(l mod 2) in {1, -i} (a lane-selected
     // swap and sign on the ALU pipe), a packed complex multiply from stage 2 on
     template <int K>
