@@ -66,6 +66,17 @@ __device__ __forceinline__ float2 cmul2(float2 v, float2 w) {
     const float2 t = cscale(v, w.y);
     return cfma(w.x, v, make_float2(-t.y, t.x));
 }
+#ifndef FPM_CMUL_PACKED
+#define FPM_CMUL_PACKED 1  // complex products as FMUL2 + FFMA2 (0: four scalar FMUL / FFMA)
+#endif
+#if FPM_CMUL_PACKED
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return cmul2(a, b); }
+// a * conj(b) = b.x a + (t.y, -t.x), t = b.y a: FMUL2 + FFMA2
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    const float2 t = cscale(a, b.y);
+    return cfma(b.x, a, make_float2(t.y, -t.x));
+}
+#else
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
@@ -73,6 +84,7 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
+#endif
 __device__ __forceinline__ float cabs2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
 
 // Single-MUFU approximations without the denormal pre/post scaling of the
