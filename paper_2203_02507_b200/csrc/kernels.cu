@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                     const float sc = meas * r;
 #endif
                     // uu = conj(e n^2): undo the conjugation
-                    v[a][u] = make_float2(ux * sc, -uu.y * sc);
+                    v[a][u] = cscale(make_float2(ux, -uu.y), sc);  // one FMUL2 (.NP negates the high half)
                 }
             float den = MEAS == kMeasTMA ? float(den_u) : den_f;
 #pragma unroll
@@ -719,9 +719,9 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                         // P'_new = P' + beta conj(O) d' / max|O|^2 (s = checkerboard sign)
                         const float2 d = csub(v[Lat::a(qq)][Lat::j(qq)], cmul(O, P));
                         if (on && upd_o)
-                            cv[Lat::a(qq) * 8 * N + 16 * Lat::j(qq)] = cadd(O, cscale(cmulc(d, P), inv_pmax));
+                            cv[Lat::a(qq) * 8 * N + 16 * Lat::j(qq)] = cfma(inv_pmax, cmulc(d, P), O);
                         if constexpr (kUpdP)
-                            if (on) P_s[qq * kGroupThreads + tl] = cadd(P, cscale(cmulc(d, O), inv_omax));
+                            if (on) P_s[qq * kGroupThreads + tl] = cfma(inv_omax, cmulc(d, O), P);
                     }
                 }
                 };

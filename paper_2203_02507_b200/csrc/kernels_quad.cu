@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
                 const float dm = fmaf(m2 * rr, inv_n2, -meas);  // |e| - sqrt(I)
                 num = fmaf(dm, dm, num);
                 const float sc = meas * rr;
-                v[i][j] = make_float2(ux * sc, -uu.y * sc);
+                v[i][j] = cscale(make_float2(ux, -uu.y), sc);  // one FMUL2
             }
         float den = float(den_u);
 #pragma unroll
@@ -477,8 +477,8 @@ __global__ void __launch_bounds__(kQThreads, MINB)
                 const float2 O = Ostg[q * kQThreads + t];
                 const float2 P = P_s[q * kQThreads + t];
                 const float2 d = csub(v[1 + (q >> 1)][1 + (q & 1)], cmul(O, P));
-                if (on && upd_o) cv[(q >> 1) * 16 * N + 16 * (q & 1) + 16 * N + 16] = cadd(O, cscale(cmulc(d, P), inv_pmax));
-                if (on && upd_p) P_s[q * kQThreads + t] = cadd(P, cscale(cmulc(d, O), inv_omax));
+                if (on && upd_o) cv[(q >> 1) * 16 * N + 16 * (q & 1) + 16 * N + 16] = cfma(inv_pmax, cmulc(d, P), O);
+                if (on && upd_p) P_s[q * kQThreads + t] = cfma(inv_omax, cmulc(d, O), P);
             }
         }
         __syncthreads();  // canvas writes visible to the next update's gather; buffers free
