@@ -66,6 +66,12 @@ __device__ __forceinline__ float2 cmul2(float2 v, float2 w) {
     const float2 t = cscale(v, w.y);
     return cfma(w.x, v, make_float2(-t.y, t.x));
 }
+// conj(v p) in two packed instructions: s = p.x v, then (s.x, -s.y) - p.y swap(v)
+// (FFMA2 with a negated broadcast, a swapped multiplicand and a half-negated addend)
+__device__ __forceinline__ float2 cmul_conj(float2 v, float2 p) {
+    const float2 s = cscale(v, p.x);
+    return cfma(-p.y, make_float2(v.y, v.x), make_float2(s.x, -s.y));
+}
 #ifndef FPM_CMUL_PACKED
 #define FPM_CMUL_PACKED 1  // complex products as FMUL2 + FFMA2 (0: four scalar FMUL / FFMA)
 #endif

@@ -550,8 +550,8 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
             }
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
-                const float2 c = cmul(v[Lat::a(q)][Lat::j(q)], P_s[q * kGroupThreads + tl]);
-                v[Lat::a(q)][Lat::j(q)] = make_float2(c.x, -c.y);  // conj: the IFFT runs as conj(FFT(conj x))
+                // conj: the IFFT runs as conj(FFT(conj x))
+                v[Lat::a(q)][Lat::j(q)] = cmul_conj(v[Lat::a(q)][Lat::j(q)], P_s[q * kGroupThreads + tl]);
             }
 
             // ---- pass 0: centered inverse transform (unscaled; 1/n^2 enters only the residual),

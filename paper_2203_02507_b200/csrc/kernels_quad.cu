@@ -380,8 +380,7 @@ __global__ void __launch_bounds__(kQThreads, MINB)
 #pragma unroll
         for (int q = 0; q < kQNP; ++q) {
             float2& x = v[1 + (q >> 1)][1 + (q & 1)];
-            const float2 c = cmul(x, P_s[q * kQThreads + t]);
-            x = make_float2(c.x, -c.y);
+            x = cmul_conj(x, P_s[q * kQThreads + t]);
         }
 
         // ---- centred inverse transform (unscaled), modulus replacement
