@@ -47,6 +47,14 @@ __device__ __forceinline__ float2 cfma(float s, float2 a, float2 b) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(make_float2(s, s))), "l"(pk(a)), "l"(pk(b)));
     return upk(r);
 }
+// s * a + b with a per-half multiplier s = (s.x, s.y): for the lane rotations
+// (x + k y, y - k x) = (k, -k) swap(x) + x, one FFMA2 (the (k, -k) pair is the
+// broadcast k with a half negation, the swap an operand modifier)
+__device__ __forceinline__ float2 cfma_v(float2 s, float2 a, float2 b) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(s)), "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
 __device__ __forceinline__ float2 cscale(float2 a, float s) {
     f32x2 r;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(make_float2(s, s))));

@@ -188,9 +188,9 @@ __device__ __forceinline__ void fft_first(float2 (&v)[8][4], float2* T_s, const 
 #if FPM_PAIR_ROT
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
-        v[a][1] = cfma(kh, make_float2(v[a][1].y, -v[a][1].x), v[a][1]);  // odd: R1 = (x + y, y - x)
+        v[a][1] = cfma_v(make_float2(kh, -kh), make_float2(v[a][1].y, v[a][1].x), v[a][1]);  // odd: R1 = (x + y, y - x)
         v[a][2] = mul_mi_odd(v[a][2], h);
-        v[a][3] = cfma(kh, make_float2(-v[a][3].y, v[a][3].x), v[a][3]);  // odd: -R3 = (x - y, x + y)
+        v[a][3] = cfma_v(make_float2(-kh, kh), make_float2(v[a][3].y, v[a][3].x), v[a][3]);  // odd: -R3 = (x - y, x + y)
         v[a][0] = cfma(sg, v[a][0], shfl_pair(v[a][0]));  // E + O | E - O
         v[a][1] = cfma(c1, v[a][1], shfl_pair(v[a][1]));  // sqrt(2) E + R1 | E - s R1
         v[a][2] = cfma(sg, v[a][2], shfl_pair(v[a][2]));

@@ -76,9 +76,9 @@ __device__ __forceinline__ PairK pair_k(int h) {
 // W8^1, W8^3 are rotations R (one FFMA2 on the odd lane) whose 1/sqrt(2) the odd
 // lane applies in the combine and the even lane defers to the step-1 twiddle.
 __device__ __forceinline__ void dit_pair(float2& w0, float2& w1, float2& w2, float2& w3, int xm, const PairK& k) {
-    w1 = cfma(k.kh, make_float2(w1.y, -w1.x), w1);  // odd: R1 = (x + y, y - x) = sqrt(2) W8 x
+    w1 = cfma_v(make_float2(k.kh, -k.kh), make_float2(w1.y, w1.x), w1);  // odd: R1 = (x + y, y - x) = sqrt(2) W8 x
     w2 = mul_mi_h(w2, k.h);
-    w3 = cfma(k.kh, make_float2(-w3.y, w3.x), w3);  // odd: (x - y, x + y) = -sqrt(2) W8^3 x
+    w3 = cfma_v(make_float2(-k.kh, k.kh), make_float2(w3.y, w3.x), w3);  // odd: (x - y, x + y) = -sqrt(2) W8^3 x
     w0 = cfma(k.sg, w0, shfl_x(w0, xm));
     w1 = cfma(k.c1, w1, shfl_x(w1, xm));
     w2 = cfma(k.sg, w2, shfl_x(w2, xm));
@@ -92,9 +92,9 @@ __device__ __forceinline__ void dif_pair(float2& x0, float2& x1, float2& x2, flo
     x1 = cfma(k.sg, x1, shfl_x(x1, xm));
     x2 = cfma(k.sg, x2, shfl_x(x2, xm));
     x3 = cfma(k.sg, x3, shfl_x(x3, xm));
-    x1 = cscale(cfma(k.kh, make_float2(x1.y, -x1.x), x1), k.s1);  // W8 x = R1 / sqrt(2)
+    x1 = cscale(cfma_v(make_float2(k.kh, -k.kh), make_float2(x1.y, x1.x), x1), k.s1);  // W8 x = R1 / sqrt(2)
     x2 = mul_mi_h(x2, k.h);
-    x3 = cscale(cfma(k.kh, make_float2(-x3.y, x3.x), x3), k.s3);  // W8^3 x = -(x - y, x + y) / sqrt(2)
+    x3 = cscale(cfma_v(make_float2(-k.kh, k.kh), make_float2(x3.y, x3.x), x3), k.s3);  // W8^3 x = -(x - y, x + y) / sqrt(2)
 }
 
 // One forward 64 x 64 transform in the quad layout (the inverse runs as
