@@ -191,11 +191,13 @@ int cluster_choice(int n, int N, int T) {
 // 44.2 ms, tools/quad_probe.sh). Batches below 64 tiles (single tiles, small FOVs) stay
 // on the pair lattice, whose sequential runs are bit-identical to the pipelined
 // schedule (test_parallel.cpp:97-108). FPM_B200_QUAD=1|0 forces.
+// The quad-lattice kernel is opt-in (FPM_B200_QUAD=1): since the packed-operand
+// rewrites, the 255-register pair build is faster at one tile per SM too
+// (profiles/r2/strong_probe.txt: 128 tiles 6.97 vs 7.55 ms, 64 tiles 6.84 vs 7.45 ms).
 bool quad_choice(int T) {
+    (void)T;
     if (const char* e = std::getenv("FPM_B200_QUAD"); e && e[0]) return e[0] == '1';
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return T >= 64 && T <= sms;
+    return false;
 }
 
 std::vector<float2> twiddles(int N) {
