@@ -298,6 +298,8 @@ __global__ void __launch_bounds__(512, FPM_LINES_BOX_MINB) lines_box_w256(const 
     // x n columns; final cols: n rows x <= 6 LR columns), staged once
     constexpr int kSq = 1536;
     __shared__ float sq[(WHICH == 0 || WHICH == 3) ? kSq : 1];
+    __shared__ int2 rowab[WHICH == 3 ? NL : 1];
+    __shared__ float rowwy[WHICH == 3 ? NL : 1];
     int wy0 = 0, wx0 = 0, wsw = 0;
     bool sq_on = false;
     auto lr_lo = [&](int hr0) { return max(int(floorf((hr0 + 0.5f) / a.up - 0.5f)), 0); };
@@ -318,6 +320,16 @@ __global__ void __launch_bounds__(512, FPM_LINES_BOX_MINB) lines_box_w256(const 
         }
         wsw = wx1 - wx0 + 1;
         sq_on = (wy1 - wy0 + 1) * wsw <= kSq;
+        if (WHICH == 3) {  // per output row: sq offsets of its two LR taps and the y weight
+            for (int k = threadIdx.x; k < NL; k += blockDim.x) {
+                const float fy = (k + 0.5f) / a.up - 0.5f;
+                int ya = int(floorf(fy));
+                rowwy[k] = fy - ya;
+                const int yb = min(ya + 1, n - 1) - wy0;
+                ya = max(ya, 0) - wy0;
+                rowab[k] = make_int2(ya * wsw, yb * wsw);
+            }
+        }
         if (sq_on) {
             const int2 txy = a.tile_xy[tile];
             const uint16_t* f = a.frame + size_t(txy.y) * a.pitch + txy.x;
@@ -394,16 +406,12 @@ __global__ void __launch_bounds__(512, FPM_LINES_BOX_MINB) lines_box_w256(const 
         const size_t opitch = a.out_off ? size_t(a.out_pitch) : size_t(NL);
         for (int i = threadIdx.x / LPB; i < NL; i += blockDim.x / LPB) {
             float2 x = s[line * LS + pad(i)];
-            x.y = -x.y;
             const float sc = ((i + j) & 1) ? -a.scale : a.scale;
-            x = cscale(x, sc);
-            const float fy = (i + 0.5f) / a.up - 0.5f;
-            int ya = int(floorf(fy));
-            const float wy = fy - ya;
-            const int yb = min(ya + 1, n - 1) - wy0;
-            ya = max(ya, 0) - wy0;
-            const float* q0 = sq + ya * wsw;
-            const float* q1 = sq + yb * wsw;
+            x = cscale(make_float2(x.x, -x.y), sc);  // conj folded into one FMUL2
+            const int2 yab = rowab[i];  // the row's bilinear taps and weight (staged once per block)
+            const float wy = rowwy[i];
+            const float* q0 = sq + yab.x;
+            const float* q1 = sq + yab.y;
             x.x += (1.f - wy) * ((1.f - wx) * q0[xa] + wx * q0[xb]) + wy * ((1.f - wx) * q1[xa] + wx * q1[xb]);
             a.dst[obase + size_t(i) * opitch] = x;
         }
