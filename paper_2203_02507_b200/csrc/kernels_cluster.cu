@@ -34,6 +34,9 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef FPM_CL_ST8
+#define FPM_CL_ST8 1  // n = 256: measurement slab staged by 8-byte cp.async (column XOR on groups of four)
+#endif
 #ifndef FPM_CL_ASY256
 #define FPM_CL_ASY256 0  // n = 256, one slab buffer: phase-A rows by st.async counted on an mbarrier
 #endif
@@ -297,21 +300,33 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
     // (XOR on pairs: the modulus reads of rows k0 + M t land in distinct banks); staged
     // asynchronously one update ahead by 4-byte cp.async, consumed only by phase B
     const bool even_x = ((txy.x + rank * SW) & 1) == 0;
+    // ST8 (WarpFFT256): 8-byte copies, the column XOR on groups of four (4 p): the modulus
+    // reads of one register then cover 16 bank pairs (2-way), half the copy instructions
+    constexpr bool ST8 = FPM_CL_ST8 && NLR == 256 && !STG;
+    auto isw_k = [&](int r) -> int { return (ST8 ? 4 * (r & 15) : FFT::isw(r)) & (SW - 1); };
+    const bool quad_x = ((txy.x + rank * SW) & 3) == 0 && (bx.pitch & 3) == 0 && (bx.frame_stride & 3) == 0;
     auto stage = [&](int pos) {
         const uint16_t* fr =
             bx.frames + size_t(F_s[pos]) * bx.frame_stride + size_t(txy.y) * bx.pitch + txy.x + rank * SW;
-        if (even_x) {
+        if (ST8 && quad_x) {
+            static_assert(!ST8 || NT % (SW / 4) == 0, "stage: whole rows per pass");
+            const int jq = 4 * (int(threadIdx.x) % (SW / 4));
+            const uint16_t* src = fr + jq;
+            for (int r = int(threadIdx.x) / (SW / 4); r < NLR; r += NT / (SW / 4))
+                cp_async8(I_s + r * SW + (jq ^ isw_k(r)), src + size_t(r) * bx.pitch);
+            cp_async_commit();
+        } else if (even_x) {
             // thread t: column pair t mod SW/2 of rows t / (SW/2) + k NT / (SW/2) (no division per copy)
             static_assert(NT % (SW / 2) == 0, "stage: whole rows per pass");
             const int jp = 2 * (int(threadIdx.x) % (SW / 2));
             const uint16_t* src = fr + jp;
             for (int r = int(threadIdx.x) / (SW / 2); r < NLR; r += NT / (SW / 2))
-                cp_async4(I_s + r * SW + (jp ^ (FFT::isw(r) & (SW - 1))), src + size_t(r) * bx.pitch);
+                cp_async4(I_s + r * SW + (jp ^ isw_k(r)), src + size_t(r) * bx.pitch);
             cp_async_commit();
         } else {
             for (int idx = threadIdx.x; idx < NLR * SW; idx += NT) {
                 const int r = idx / SW, jj = idx % SW;
-                I_s[r * SW + (jj ^ (FFT::isw(r) & (SW - 1)))] = fr[size_t(r) * bx.pitch + jj];
+                I_s[r * SW + (jj ^ isw_k(r))] = fr[size_t(r) * bx.pitch + jj];
             }
         }
     };
@@ -471,7 +486,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             }
             F.f1(x);  // = conj(e), e the unscaled 2-D IFFT
             // every row this lane holds shares one column swizzle (FFT::isw_lane)
-            const uint16_t* Ic = I_s + (jj ^ (F.isw_lane() & (SW - 1)));
+            const uint16_t* Ic = I_s + (jj ^ ((ST8 ? 4 * (l & 15) : F.isw_lane()) & (SW - 1)));
 #pragma unroll
             for (int k0 = 0; k0 < M; ++k0) {
                 const int row = F.scr(k0);
