@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
     // reads of one register then cover 16 bank pairs (2-way), half the copy instructions
     constexpr bool ST8 = FPM_CL_ST8 && NLR == 256 && !STG;
     auto isw_k = [&](int r) -> int { return (ST8 ? 4 * (r & 15) : FFT::isw(r)) & (SW - 1); };
-    const bool quad_x = ((txy.x + rank * SW) & 3) == 0 && (bx.pitch & 3) == 0 && (bx.frame_stride & 3) == 0;
+    const bool quad_x = ((txy.x + rank * SW) & 3) == 0 && (bx.pitch & 3) == 0 && (bx.frame_stride & 3) == 0 &&
+                        (reinterpret_cast<uintptr_t>(bx.frames) & 7) == 0;  // every copy source 8-byte aligned
     auto stage = [&](int pos) {
         const uint16_t* fr =
             bx.frames + size_t(F_s[pos]) * bx.frame_stride + size_t(txy.y) * bx.pitch + txy.x + rank * SW;
