@@ -72,6 +72,9 @@ __device__ __forceinline__ float4 tw_entry(double c, double s) {
 #ifndef FPM_SUM_LANE
 #define FPM_SUM_LANE 0  // thread (of the group) that adds the update's residual ratio
 #endif
+#ifndef FPM_DEN_SEP
+#define FPM_DEN_SEP 1  // sum(I) of a crop by a separate loop on first visits (not a predicated add per pixel)
+#endif
 #ifndef FPM_TW2
 #define FPM_TW2 1  // twiddle tables as float2 with the two-instruction cmul2 (0: float4 (w, iw) pairs, cmul_sw)
 #endif
@@ -582,7 +585,7 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                     if (MEAS == kMeasTMA) {
                         // FPM_MEAS_SWIZZLE: 16-byte chunk b of row i sits at chunk b ^ (i & 7), i & 7 == tr
                         const uint32_t Iu = I_s[(tr + 8 * a) * 64 + ((FPM_MEAS_SWIZZLE ? b ^ tr : b) << 3) + tc];
-                        if (first) den_u += Iu;
+                        if (!FPM_DEN_SEP && first) den_u += Iu;
                         Iv = float(Iu);
                     } else {
                         Iv = args.meas_f32[(tr + 8 * a) * 64 + tc + 8 * b];
@@ -614,6 +617,13 @@ __global__ void __launch_bounds__(kGroupThreads * G, G == 1 ? MINB : 2)
                     // uu = conj(e n^2): undo the conjugation
                     v[a][u] = cscale(make_float2(ux, -uu.y), sc);  // one FMUL2 (.NP negates the high half)
                 }
+            if (FPM_DEN_SEP && MEAS == kMeasTMA && first) {  // sum(I): a separate pass on first visits only
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        den_u += I_s[(tr + 8 * a) * 64 + (((FPM_MEAS_SWIZZLE ? (2 * u + h) ^ tr : 2 * u + h)) << 3) + tc];
+            }
             float den = MEAS == kMeasTMA ? float(den_u) : den_f;
 #pragma unroll
             for (int sh = 16; sh; sh >>= 1) num += __shfl_xor_sync(kFull, num, sh);
