@@ -582,8 +582,10 @@ void plan_loop(fpmgpu_plan& p, const uint16_t* frames, int64_t pitch, double* re
         bx.box = p.box;
         bx.b0 = p.b0;
         bx.sup_rows = p.sup_rows.p;
-        if (p.cl && p.G == 1 && s0 == 0 && s1 == p.num_slots && !acc)  // whole run: the work queue may serve it
+        if (p.cl && p.G == 1 && s0 == 0 && s1 == p.num_slots && !acc) {  // whole run: the work queue may serve it
             a.work = p.work.ensure(size_t(p.T) + 1);
+            a.isum = p.isum.ensure(size_t(p.T) * p.L);  // sum(I) per (tile, LED), formed on pass 0
+        }
         if (p.cl)
             ck(fpmk::launch_loop_cluster(p.n, r.mode, p.cl, a, bx, p.T, s), "LED loop (cluster)");
         else

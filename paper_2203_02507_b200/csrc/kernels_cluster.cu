@@ -34,6 +34,9 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef FPM_CL_DENSEP
+#define FPM_CL_DENSEP 1  // whole runs: sum(I) formed on pass 0 only (a separate loop), cached per (tile, LED)
+#endif
 #ifndef FPM_CL_ST8
 #define FPM_CL_ST8 1  // n = 256: measurement slab staged by 8-byte cp.async (column XOR on groups of four)
 #endif
@@ -476,6 +479,8 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
         }
 
         // ---- B: this CTA's columns: IFFT over the box rows -> modulus -> FFT -> box rows
+        // (sum(I): on pass 0 of a whole run, or every update without the per-(tile, LED) cache)
+        const bool den_now = !FPM_CL_DENSEP || args.isum == nullptr || it == 0;
         float num = 0.f, den = 0.f;
         for (int jj = w; jj < SW; jj += NW) {
             const int j = rank * SW + jj;
@@ -493,7 +498,7 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 const int row = F.scr(k0);
                 FPM_ASSERT(row >= 0 && row < NLR && (Ic - I_s) + row * SW < SW * NLR);
                 const float Iv = float(Ic[row * SW]);
-                den += Iv;
+                if (!FPM_CL_DENSEP) den += Iv;
                 // |e| = 0 rule (recon.cpp:122) as in fpm_loop64: Re nudged by sgn 2^-60 maps
                 // e = 0 to e' = sgn sqrt(I) (checkerboard sign), leaves |Re| >= 2^-35 exact
                 const float meas = sqrt_ftz(Iv);
@@ -506,6 +511,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 const float sc = meas * rr;
                 x[k0] = make_float2(ux * sc, -u.y * sc);  // e' from u = conj(e)
             }
+            if (FPM_CL_DENSEP && den_now) {  // the same additions in the same order, pass 0 only
+#pragma unroll
+                for (int k0 = 0; k0 < M; ++k0) den += float(Ic[F.scr(k0) * SW]);
+            }
             F.f2(x);
 #pragma unroll
             for (int r = 0; r < M; ++r) {
@@ -514,9 +523,10 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
             }
         }
 #pragma unroll
-        for (int sh = 16; sh; sh >>= 1) {
-            num += __shfl_xor_sync(kFull, num, sh);
-            den += __shfl_xor_sync(kFull, den, sh);
+        for (int sh = 16; sh; sh >>= 1) num += __shfl_xor_sync(kFull, num, sh);
+        if (den_now) {
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) den += __shfl_xor_sync(kFull, den, sh);
         }
         if (l == 0) {
             wred[w * 4] = num;
@@ -567,7 +577,16 @@ __global__ void __launch_bounds__(NW * 32, NLR <= 128 ? 16 / NW : 512 / (NW * 32
                 a3 = fmaxf(a3, __shfl_xor_sync(kFull, a3, sh));
             }
             if (l == 0) {
-                if (rank == 0) stage_sum[it] += a1 > 0.f ? double(__fdividef(a0, a1)) : 0.0;  // as fpm_loop64
+                if (rank == 0) {
+                    if (FPM_CL_DENSEP && args.isum) {  // pass 0 stores the crop's sum(I), later passes read it
+                        float* is = args.isum + size_t(tile) * L + pos;
+                        if (den_now)
+                            *is = a1;
+                        else
+                            a1 = *is;
+                    }
+                    stage_sum[it] += a1 > 0.f ? double(__fdividef(a0, a1)) : 0.0;  // as fpm_loop64
+                }
                 upd[0] = (a2 > 0.f && bright) ? args.beta / a2 : 0.f;  // bright-field pupil steps only
                 if (want_p) upd[1] = a3 > 0.f ? args.alpha / a3 : 0.f;  // else the pupil's value stands
             }
